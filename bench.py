@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the EVP ternary kNN hot path on B200 (BASELINE.json metric:
+query x db Delta-evals/s and kNN QPS; % of roofline).
+
+One step = one pass of the whole hot path over one query batch of the
+workload: encode the Q query embeddings (uq_encode), scan all N database codes
+with the fused per-query top-k (uq_search: scan kernel + merge kernel), and for
+N GPUs the NCCL allgather of the [Q][k] lists + uq_merge_topk.  The database is
+encoded once before timing (index build, "pre-processing of S before q
+becomes available"); that encode is reported separately under "encode".
+
+Default workload: BASELINE config 2 (d=768, N=1e6, Q=1000, x=384, k=100,
+single GPU).  Multi-GPU (torchrun): weak scaling, each rank holds an N-row
+shard of the global database (rows [r*N, (r+1)*N) of the same seeded stream).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--algo auto]
+    python bench.py --impl reference ...   # the CPU oracle on the same workload
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import datagen  # noqa: E402
+
+METRIC = "query x db Delta-evals/s (kNN over {x,d} EVP ternary codes)"
+UNIT = "delta_evals/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _popc_peak():
+    """POPC/clk/SM measured by tools/peaks.cu on a B200 (profiles/peaks_r01.json)."""
+    p = os.path.join(ROOT, "profiles", "peaks_r01.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["popc_per_clk_sm_at_attr_clock"]), "measured (tools/peaks.cu)"
+    return 16.0, "assumed 16/clk/SM (CUDA Programming Guide cc 7.x-9.0 value)"
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return world, rank, local
+
+
+def _barrier(world):
+    if world > 1:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference): the oracle as it stands
+# ---------------------------------------------------------------------------
+def _oracle_sample(w, target_s: float):
+    """Time the oracle's encode(queries) + exhaustive kNN on a bounded sample of
+    the workload: n_s database rows (oracle-encoded, untimed) x q_s queries."""
+    import oracle
+    n_s = min(w.n, 20000)
+    db = datagen.db(w, "cpu", 0, n_s).numpy()
+    q_all = datagen.rows(w, "q", 0, min(w.nq, 256), "cpu").numpy()
+    o_db = oracle.pack(oracle.encode(db, w.x))
+
+    def run(nq_s):
+        t0 = time.perf_counter()
+        o_q = oracle.pack(oracle.encode(q_all[:nq_s], w.x))
+        oracle.knn(o_q, o_db, w.d, w.k)
+        return time.perf_counter() - t0
+
+    t1 = run(1)
+    cores = os.cpu_count() or 1
+    nq_s = int(max(1, min(q_all.shape[0], target_s / max(t1, 1e-6) * min(cores, 8))))
+    return n_s, nq_s, run, cores
+
+
+def cpu_baseline(w, target_s=10.0):
+    n_s, nq_s, run, cores = _oracle_sample(w, target_s)
+    t = run(nq_s)
+    return {"value": nq_s * n_s / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{nq_s} queries (oracle encode + exhaustive kNN, k={w.k}) over the first "
+                      f"{n_s} database rows of {w.name}; {t:.1f} s wall on {cores} host threads"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    w = datagen.CONFIGS[args.config]
+    n_s, nq_s, run, cores = _oracle_sample(w, target_s=2.0)
+    for _ in range(args.warmup):
+        run(nq_s)
+    times = [run(nq_s) for _ in range(args.steps)]
+    tot = sum(times)
+    value = args.steps * nq_s * n_s / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": _workload_desc(w), "sample": f"{nq_s} queries x {n_s} rows per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{nq_s} queries x first {n_s} rows of {w.name} per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _workload_desc(w):
+    return (f"{w.name}: d={w.d}, N={w.n}, Q={w.nq}, x={w.x}, k={w.k}, {w.kind}"
+            f"{' C=' + str(w.centres) if w.centres else ''}, {str(w.dtype).replace('torch.', '')}"
+            f"{', l2-normalised' if w.normalise else ', raw'}")
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(datagen.CONFIGS))
+    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc"])
+    ap.add_argument("--n", type=int, default=None, help="override DB rows per GPU")
+    ap.add_argument("--nq", type=int, default=None, help="override query batch")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = _dist()
+    if args.impl == "reference":
+        rc = run_reference(args, world, rank)
+        if world > 1:
+            dist.destroy_process_group()
+        return rc
+
+    import paper_2506_00528_b200 as uq
+    from paper_2506_00528_b200.parallel import allgather_lists
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = datagen.CONFIGS[args.config].scaled(n=args.n, nq=args.nq)
+    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05}[args.algo]
+    n_loc, nq, d, x, k = w.n, w.nq, w.d, w.x, w.k
+    id_base = rank * n_loc
+
+    # ---- data (seeded, synthetic; DB shard + replicated queries) ----
+    u_db = datagen.rows(w, "db", id_base, n_loc, dev)
+    u_q = datagen.queries(w, dev)
+    u_q_host = u_q.cpu().pin_memory()
+    torch.cuda.synchronize()
+
+    # ---- index build: encode the DB shard once (timed separately) ----
+    dbc = torch.empty((n_loc, uq.code_bytes(d)), dtype=torch.uint8, device=dev)
+    uq.encode(u_db, x, out=dbc)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    uq.encode(u_db, x, out=dbc)
+    e1.record()
+    torch.cuda.synchronize()
+    enc_ms = e0.elapsed_time(e1)
+    enc_bytes = n_loc * (d * u_db.element_size() + uq.code_bytes(d))
+    del u_db
+    torch.cuda.empty_cache()
+
+    qc = torch.empty((nq, uq.code_bytes(d)), dtype=torch.uint8, device=dev)
+    out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
+           torch.empty((nq, k), dtype=torch.int64, device=dev))
+    ws = torch.empty(max(uq.search_workspace(nq, n_loc, d, k, algo), 1), dtype=torch.uint8,
+                     device=dev)
+    launches = [0]
+
+    def step(q_dev):
+        uq.encode(q_dev, x, out=qc)
+        launches[0] += uq.last_launches()
+        s, i = uq.search(qc, dbc, d, k, id_base=id_base, algo=algo, workspace=ws, out=out)
+        launches[0] += uq.last_launches()
+        if world > 1:
+            sg, ig = allgather_lists(s, i)
+            s, i = uq.merge_topk(sg, ig, k)
+            launches[0] += uq.last_launches()
+        return s, i
+
+    for _ in range(args.warmup):
+        step(u_q)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches[0] = 0
+    uq.timing_enable(True)
+    _barrier(world)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step(u_q)
+    t1.record()
+    torch.cuda.synchronize()
+    _barrier(world)
+    uq.timing_enable(False)
+    clk = clocks.stop()
+    gpu_launches = launches[0]
+    ms = t0.elapsed_time(t1)
+    scan_ms, scan_n = uq.timing_collect()
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # ---- end to end through the public API: pinned host queries in, results out ----
+    host_s = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    host_i = torch.empty((nq, k), dtype=torch.int64).pin_memory()
+    q_stage = torch.empty_like(u_q)
+    _barrier(world)
+    torch.cuda.synchronize()
+    t2, t3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t2.record()
+    for _ in range(args.steps):
+        q_stage.copy_(u_q_host, non_blocking=True)
+        s, i = step(q_stage)
+        host_s.copy_(s, non_blocking=True)
+        host_i.copy_(i, non_blocking=True)
+    t3.record()
+    torch.cuda.synchronize()
+    _barrier(world)
+    e2e_ms = t2.elapsed_time(t3)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    evals_per_step = nq * n_loc * world
+    value = evals_per_step * args.steps / (ms * 1e-3)
+    e2e_value = evals_per_step * args.steps / (e2e_ms * 1e-3)
+
+    peaks, peaks_src = _peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    used_tc = (algo == uq.ALGO_TCGEN05) or (algo == uq.ALGO_AUTO and _auto_is_tc(uq, nq, n_loc, d, k))
+    scan_avg_s = (scan_ms / max(scan_n, 1)) * 1e-3
+    if used_tc:
+        # int8 MACs: d per Delta (the int8 GEMM T_q . T_db^T), 2 ops per MAC
+        ops = 2.0 * d * nq * n_loc
+        peak = 2.0 * float(peaks["bf16_tflops"])   # int8 dense = 2x bf16 (guide's nominal ratio)
+        achieved = ops / scan_avg_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "scan_tc_kernel (int8 tcgen05 Delta GEMM + fused top-k)",
+                "peak_source": f"2 x bf16_tflops of {peaks_src} MEASURED_PEAKS.json (int8 = 2x bf16 nominal)",
+                "algorithmic": "2*d ops per Delta (d int8 MACs)"}
+    else:
+        popc_clk, popc_src = _popc_peak()
+        popc_per_delta = 2.0 * ((d + 31) // 32)   # identity: 2 POPC per 32-bit word
+        achieved = popc_per_delta * nq * n_loc / scan_avg_s / 1e12
+        peak = popc_clk * sms * sm_mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tpopc/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "scan_popc_kernel (LOP3+POPC Delta scan + fused top-k)",
+                "peak_source": f"{popc_clk:.2f} POPC/clk/SM {popc_src} x {sms} SMs x {sm_mhz:.0f} MHz",
+                "algorithmic": "2*ceil(d/32) POPC per Delta"}
+    roof["scan_ms_avg"] = scan_avg_s * 1e3
+    roof["scan_share_of_step"] = (scan_ms / max(ms, 1e-9)) if world == 1 else None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "s8" if used_tc else "u32",
+        "data": "synthetic",
+        "config": {"workload": _workload_desc(w), "db_rows_per_gpu": n_loc, "global_db_rows": n_loc * world,
+                   "queries": nq, "k": k, "algo": "tcgen05" if used_tc else "popc",
+                   "parallelism": f"db-shard x{world} + allgather/merge" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2: {n_loc * uq.code_bytes(d) / 1e6:.0f} MB of DB codes per GPU scanned per step"},
+        "qps": nq * args.steps / (ms * 1e-3),
+        "roofline": roof,
+        "encode": {"rows_per_s": n_loc / (enc_ms * 1e-3), "GB_per_s": enc_bytes / (enc_ms * 1e-3) / 1e9,
+                   "hbm_frac": enc_bytes / (enc_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"]),
+                   "ms": enc_ms, "note": "DB index build, outside the step"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "qps": nq * args.steps / (e2e_ms * 1e-3),
+                "h2d_bytes_per_step": u_q.numel() * u_q.element_size(),
+                "d2h_bytes_per_step": nq * k * (4 + 8)},
+        "gpu_launches": gpu_launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _auto_is_tc(uq, nq, n, d, k):
+    try:
+        return uq.search_workspace(nq, n, d, k, uq.ALGO_TCGEN05) > 0 and nq >= 64
+    except uq.UQError:
+        return False
+
+
+if __name__ == "__main__":
+    sys.exit(main())

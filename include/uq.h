@@ -1,0 +1,159 @@
+/*
+ * uq.h -- C ABI of libuq.so: B200 (sm_100a) brute-force kNN over {x,d} EVP
+ * ternary codes (arXiv 2506.00528, "Ultra-Quantisation: Efficient Embedding
+ * Search via 1.58-bit Encodings").  Citations: P:NNN = PAPER.md line.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer is a CUDA DEVICE pointer unless marked "host".  The caller
+ *    owns every buffer; the library allocates nothing and keeps no state beyond
+ *    cached device attributes, so calls are thread-safe and reentrant.
+ *  - Every call is stream-ordered and asynchronous on `stream` (0 = legacy
+ *    default stream).  Device faults surface at the caller's next sync.
+ *  - Argument checks are synchronous and return before any launch:
+ *      UQ_ERR_INVALID_ARG  null pointer with a non-empty extent, n/nq < 0,
+ *                          d < 1, x outside [1,d], k < 1, ld < d,
+ *                          misaligned pointer (codes: 16 B; u: element size);
+ *      UQ_ERR_UNSUPPORTED  beyond compiled limits: d > UQ_MAX_D, k > UQ_MAX_K,
+ *                          n >= 2^32-1 rows in one call;
+ *      UQ_ERR_WORKSPACE    workspace smaller than uq_search_workspace();
+ *      UQ_ERR_CUDA         a launch / attribute call failed.
+ *  - Preconditions NOT checked: inputs are finite; codes are valid (pos AND
+ *    neg = 0, pad bits 0) -- uq_check_codes() verifies them on demand.
+ *
+ * Code layout (one row = code_bytes = 2 * plane_bytes bytes, 16-B aligned):
+ *    [ pos plane : plane_bytes ][ neg plane : plane_bytes ],
+ *    plane_bytes = 16 * ceil(d / 128);  bit i of a plane is bit (i % 8) of
+ *    byte (i / 8) (LSB first); pos bit i <=> v_i = +1, neg bit i <=> v_i = -1
+ *    (the v+ / v- planes of P:357); bits i >= d are 0.
+ *
+ * Ranking: Delta = b2sp(q, r), the integer ternary scalar product;
+ * larger is more similar (negative scalar product ~ l2 distance).  Ties
+ * in Delta go to the lower id.  Results are sorted best first.
+ */
+#ifndef UQ_H_
+#define UQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* uq_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  UQ_OK = 0,
+  UQ_ERR_INVALID_ARG = 1,
+  UQ_ERR_UNSUPPORTED = 2,
+  UQ_ERR_CUDA = 3,
+  UQ_ERR_WORKSPACE = 4
+} uq_status;
+
+typedef enum { UQ_F32 = 0, UQ_F16 = 1, UQ_BF16 = 2 } uq_dtype;
+
+/* Scan engine selection for uq_search_ex (uq_search uses UQ_ALGO_AUTO). */
+typedef enum {
+  UQ_ALGO_AUTO = 0,    /* tensor path for large query batches, popcount otherwise */
+  UQ_ALGO_POPC = 1,    /* LOP3 + POPC scan on CUDA cores                          */
+  UQ_ALGO_TCGEN05 = 2  /* int8 tcgen05 GEMM (UTCIMMA) with fused top-k            */
+} uq_algo;
+
+#define UQ_MAX_D 2048
+#define UQ_MAX_K 1024
+
+/* Bytes of one packed code row: 2 * 16 * ceil(d/128).  0 if d < 1. */
+size_t uq_code_bytes(int32_t d);
+
+/* Static string for a status code (never NULL). */
+const char* uq_status_str(uq_status s);
+
+/* Library version string, e.g. "uq 0.1 sm_100a". */
+const char* uq_version(void);
+
+/*
+ * uq_encode -- nearest {x,d} EVP vertex of each row, packed.
+ *   u      [n][ld_elems] row-major, element type dt (f32 / f16 / bf16).
+ *          Encoded on raw values (no normalisation: the top-x order is scale
+ *          invariant), comparing |u_i| exactly (IEEE abs bits).
+ *   x      number of non-zeros, 1 <= x <= d.  Ties in |u_i| go to the
+ *          lower index i; a selected exact zero (or -0.0) encodes as 0.
+ *   codes  [n][uq_code_bytes(d)] output, 16-B aligned.
+ */
+uq_status uq_encode(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld_elems,
+                    int32_t x, uint8_t* codes, uq_stream_t stream);
+
+/*
+ * uq_scores -- dense Delta matrix (test/debug): out[q][r] = b2sp(qcodes[q],
+ * dbcodes[r]), int32, row-major [nq][n].
+ */
+uq_status uq_scores(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n,
+                    int32_t d, int32_t* out, uq_stream_t stream);
+
+/*
+ * uq_search_workspace -- bytes of device workspace uq_search needs for this
+ * shape on the CURRENT device (*bytes is a host pointer).
+ */
+uq_status uq_search_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes);
+uq_status uq_search_workspace_ex(int64_t nq, int64_t n, int32_t d, int32_t k, uq_algo algo,
+                                 size_t* bytes);
+
+/*
+ * uq_search -- exhaustive kNN in the proxy space (P:61 problem statement;
+ * P:480 "exhaustive queries over the whole data").  For every query q: Delta
+ * against every row r of dbcodes, keep the k best under (Delta desc, id asc),
+ * write them best first:
+ *   out_scores [nq][k] int32 Delta,   out_ids [nq][k] int64 id = id_base + r.
+ * If n < k the tail of each row is (INT32_MIN, -1).  The result is unique
+ * (total order), hence identical for every engine, launch shape and sharding.
+ *   workspace  device scratch of >= uq_search_workspace() bytes, 256-B aligned.
+ */
+uq_status uq_search(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n,
+                    int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
+                    int64_t* out_ids, void* workspace, size_t workspace_bytes,
+                    uq_stream_t stream);
+uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n,
+                       int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
+                       int64_t* out_ids, void* workspace, size_t workspace_bytes, uq_algo algo,
+                       uq_stream_t stream);
+
+/*
+ * uq_merge_topk -- merge g sorted-or-unsorted candidate lists per query (e.g.
+ * the per-GPU results of a sharded search after an allgather) into the k best
+ * under (score desc, id asc):
+ *   scores [g][nq][k] int32, ids [g][nq][k] int64 (entries with id < 0 are
+ *   padding and ignored; ids must be < 2^32 - 1 and distinct per query),
+ *   out_scores / out_ids [nq][k], best first, padded with (INT32_MIN, -1).
+ * Exact because the global top-k is a subset of the union of shard top-k's.
+ */
+uq_status uq_merge_topk(const int32_t* scores, const int64_t* ids, int32_t g, int64_t nq,
+                        int32_t k, int32_t* out_scores, int64_t* out_ids, uq_stream_t stream);
+
+/*
+ * uq_check_codes -- count rows that are not valid packed ternary codes: some
+ * position set in both planes (pos AND neg != 0), or a pad bit (i >= d) set.
+ * *bad_rows is a DEVICE uint64 scalar that the call overwrites.
+ */
+uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d,
+                         unsigned long long* bad_rows, uq_stream_t stream);
+
+/*
+ * Device-side timing of the scan kernels (the dominant kernel of uq_search), for
+ * roofline accounting.  While enabled on a host thread, each scan launch issued
+ * from that thread is bracketed by CUDA events on its stream.  collect() waits
+ * for the recorded events, returns the summed kernel time (*scan_ms, host) and
+ * the number of timed launches (*launches, host), and resets the record.
+ */
+uq_status uq_timing_enable(int32_t on);
+uq_status uq_timing_collect(double* scan_ms, int64_t* launches);
+
+/*
+ * uq_last_launches -- number of kernels the most recent uq_* call on this
+ * host thread enqueued (for launch accounting in benchmarks).
+ */
+int32_t uq_last_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UQ_H_ */

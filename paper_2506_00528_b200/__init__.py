@@ -1,0 +1,192 @@
+"""uq -- B200-native brute-force kNN over {x,d} EVP ternary codes (arXiv 2506.00528).
+
+Thin Python binding over the C ABI of ``libuq.so`` (``include/uq.h``): argument
+marshalling only.  Every step of the path (encode, Delta scan, top-k, merge)
+runs in the library's sm_100a kernels; PyTorch provides device memory, streams
+and process groups.  There is no CPU fallback: importing this package without
+the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import torch
+
+__all__ = [
+    "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
+    "search_workspace", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05",
+    "last_launches", "version", "timing_enable", "timing_collect",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libuq.so")
+
+ALGO_AUTO, ALGO_POPC, ALGO_TCGEN05 = 0, 1, 2
+_DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
+_STATUS = {0: "UQ_OK", 1: "UQ_ERR_INVALID_ARG", 2: "UQ_ERR_UNSUPPORTED", 3: "UQ_ERR_CUDA",
+           4: "UQ_ERR_WORKSPACE"}
+
+
+class UQError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        super().__init__(f"{fn} failed: {_STATUS.get(status, status)}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"libuq.so not found at {_LIB_PATH}: build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    L = ctypes.CDLL(_LIB_PATH)
+    i32, i64, vp, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+    L.uq_code_bytes.argtypes, L.uq_code_bytes.restype = [i32], sz
+    L.uq_version.argtypes, L.uq_version.restype = [], ctypes.c_char_p
+    L.uq_last_launches.argtypes, L.uq_last_launches.restype = [], i32
+    L.uq_encode.argtypes = [vp, i32, i64, i32, i64, i32, vp, vp]
+    L.uq_scores.argtypes = [vp, i64, vp, i64, i32, vp, vp]
+    L.uq_search_workspace_ex.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz)]
+    L.uq_search_ex.argtypes = [vp, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, i32, vp]
+    L.uq_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
+    L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
+    L.uq_timing_enable.argtypes = [i32]
+    L.uq_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
+    for f in ("uq_timing_enable", "uq_timing_collect", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
+              "uq_check_codes"):
+        getattr(L, f).restype = i32
+    return L
+
+
+_L = _load()
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def version() -> str:
+    return _L.uq_version().decode()
+
+
+def last_launches() -> int:
+    """Kernels enqueued by the most recent uq_* call on this thread."""
+    return int(_L.uq_last_launches())
+
+
+def timing_enable(on: bool = True) -> None:
+    """Bracket every scan kernel launched from this thread with CUDA events."""
+    _check("uq_timing_enable", _L.uq_timing_enable(1 if on else 0))
+
+
+def timing_collect() -> Tuple[float, int]:
+    """(summed scan-kernel milliseconds, number of timed launches) since last collect."""
+    ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    _check("uq_timing_collect", _L.uq_timing_collect(ctypes.byref(ms), ctypes.byref(n)))
+    return float(ms.value), int(n.value)
+
+
+def code_bytes(d: int) -> int:
+    return int(_L.uq_code_bytes(d))
+
+
+def plane_bytes(d: int) -> int:
+    return code_bytes(d) // 2
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() > 0 else 0)
+
+
+def _check(fn: str, st: int):
+    if st != 0:
+        raise UQError(fn, st)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+
+
+def encode(u: torch.Tensor, x: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """Nearest {x,d} EVP vertex codes of the rows of ``u`` ([n][d], row stride
+    ``u.stride(0)``), packed [n][code_bytes(d)] uint8 (uq_encode)."""
+    _dev(u, "u")
+    if u.dim() != 2 or u.stride(1) != 1:
+        raise ValueError("u must be 2-D with unit column stride")
+    if u.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {u.dtype}")
+    n, d = u.shape
+    if out is None:
+        out = torch.empty((n, code_bytes(d)), dtype=torch.uint8, device=u.device)
+    _check("uq_encode", _L.uq_encode(_ptr(u), _DT[u.dtype], n, d, u.stride(0), x, _ptr(out),
+                                     _stream(stream)))
+    return out
+
+
+def scores(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
+    """Dense Delta matrix [nq][n] int32 (uq_scores; test/debug)."""
+    _dev(qcodes, "qcodes"); _dev(dbcodes, "dbcodes")
+    nq, n = qcodes.shape[0], dbcodes.shape[0]
+    out = torch.empty((nq, n), dtype=torch.int32, device=qcodes.device)
+    _check("uq_scores", _L.uq_scores(_ptr(qcodes), nq, _ptr(dbcodes), n, d, _ptr(out),
+                                     _stream(stream)))
+    return out
+
+
+def search_workspace(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> int:
+    b = ctypes.c_size_t(0)
+    _check("uq_search_workspace", _L.uq_search_workspace_ex(nq, n, d, k, algo, ctypes.byref(b)))
+    return int(b.value)
+
+
+def search(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base: int = 0,
+           algo: int = ALGO_AUTO, workspace: Optional[torch.Tensor] = None,
+           out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
+           stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Exhaustive proxy-space kNN (uq_search): (scores [nq][k] int32, ids [nq][k] int64),
+    best first under (Delta desc, id asc)."""
+    _dev(qcodes, "qcodes"); _dev(dbcodes, "dbcodes")
+    nq, n = qcodes.shape[0], dbcodes.shape[0]
+    dev = qcodes.device
+    if out is None:
+        out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
+               torch.empty((nq, k), dtype=torch.int64, device=dev))
+    need = search_workspace(nq, n, d, k, algo)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    _check("uq_search", _L.uq_search_ex(_ptr(qcodes), nq, _ptr(dbcodes), n, d, k, id_base,
+                                        _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
+                                        workspace.numel(), algo, _stream(stream)))
+    return out
+
+
+def merge_topk(scores_g: torch.Tensor, ids_g: torch.Tensor, k: int,
+               out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
+               stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Merge [g][nq][k] candidate lists into the k best per query (uq_merge_topk)."""
+    _dev(scores_g, "scores"); _dev(ids_g, "ids")
+    g, nq, kin = scores_g.shape
+    if kin != k:
+        raise ValueError("lists must hold k entries per query")
+    if out is None:
+        out = (torch.empty((nq, k), dtype=torch.int32, device=scores_g.device),
+               torch.empty((nq, k), dtype=torch.int64, device=scores_g.device))
+    _check("uq_merge_topk", _L.uq_merge_topk(_ptr(scores_g), _ptr(ids_g), g, nq, k, _ptr(out[0]),
+                                             _ptr(out[1]), _stream(stream)))
+    return out
+
+
+def check_codes(codes: torch.Tensor, d: int, stream=None) -> int:
+    """Number of invalid code rows (uq_check_codes); synchronises to read the count."""
+    _dev(codes, "codes")
+    bad = torch.zeros(1, dtype=torch.int64, device=codes.device)
+    _check("uq_check_codes", _L.uq_check_codes(_ptr(codes), codes.shape[0], d, _ptr(bad),
+                                               _stream(stream)))
+    return int(bad.item())

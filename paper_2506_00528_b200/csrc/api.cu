@@ -1,0 +1,244 @@
+// api.cu -- the C ABI of libuq.so (declared and documented in include/uq.h):
+// synchronous argument validation, launch planning, workspace carving.
+#include <cstdio>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace uq {
+
+static thread_local int g_launches = 0;
+void note_launch(int n) { g_launches += n; }
+
+// ---- optional scan timing (uq_timing_*) ----
+struct ScanTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t used = 0;
+  ~ScanTimer() {
+    for (auto& p : ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  }
+};
+static thread_local ScanTimer g_timer;
+
+static void timer_begin(cudaStream_t st, cudaEvent_t* stop) {
+  *stop = nullptr;
+  if (!g_timer.on) return;
+  if (g_timer.used == g_timer.ev.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess) return;
+    if (cudaEventCreate(&b) != cudaSuccess) { cudaEventDestroy(a); return; }
+    g_timer.ev.emplace_back(a, b);
+  }
+  auto& p = g_timer.ev[g_timer.used++];
+  cudaEventRecord(p.first, st);
+  *stop = p.second;
+}
+static void timer_end(cudaStream_t st, cudaEvent_t stop) {
+  if (stop) cudaEventRecord(stop, st);
+}
+
+static int device_sms() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> g(mu);
+  if (cache[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static uq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? UQ_OK : UQ_ERR_CUDA; }
+
+// Which scan engine runs for a shape.
+static uq_algo resolve_algo(uq_algo algo, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  if (algo == UQ_ALGO_POPC) return UQ_ALGO_POPC;
+  const TcPlan tp = plan_tc(nq, n, d, k, sms);
+  if (algo == UQ_ALGO_TCGEN05) return tp.ok ? UQ_ALGO_TCGEN05 : UQ_ALGO_AUTO /* unsupported */;
+  // AUTO: the popcount scan is POPC-issue-bound once nq exceeds ~3 (DESIGN.md
+  // roofline); the int8 tensor path wins for query batches that fill an M tile.
+  if (tp.ok && nq >= 64) return UQ_ALGO_TCGEN05;
+  return UQ_ALGO_POPC;
+}
+
+static uq_status validate_search(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n,
+                                 int32_t d, int32_t k) {
+  if (nq < 0 || n < 0 || d < 1 || k < 1) return UQ_ERR_INVALID_ARG;
+  if ((nq > 0 && q == nullptr) || (n > 0 && nq > 0 && db == nullptr)) return UQ_ERR_INVALID_ARG;
+  if ((q && !aligned16(q)) || (db && !aligned16(db))) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D || k > UQ_MAX_K) return UQ_ERR_UNSUPPORTED;
+  if (n >= (int64_t)0xffffffffLL) return UQ_ERR_UNSUPPORTED;
+  return UQ_OK;
+}
+
+static size_t workspace_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  if (nq == 0 || n == 0) return 0;
+  if (a == UQ_ALGO_TCGEN05) {
+    const TcPlan tp = plan_tc(nq, n, d, k, sms);
+    return align_up(tp.buf_bytes, 256) + align_up(tp.part_bytes, 256);
+  }
+  const PopcPlan pl = plan_popc(nq, n, d, k, sms);
+  return align_up(pl.buf_bytes, 256) + align_up(pl.part_bytes, 256);
+}
+
+}  // namespace uq
+
+using namespace uq;
+
+extern "C" {
+
+size_t uq_code_bytes(int32_t d) { return d < 1 ? 0 : (size_t)code_bytes(d); }
+
+const char* uq_status_str(uq_status s) {
+  switch (s) {
+    case UQ_OK: return "UQ_OK";
+    case UQ_ERR_INVALID_ARG: return "UQ_ERR_INVALID_ARG";
+    case UQ_ERR_UNSUPPORTED: return "UQ_ERR_UNSUPPORTED";
+    case UQ_ERR_CUDA: return "UQ_ERR_CUDA";
+    case UQ_ERR_WORKSPACE: return "UQ_ERR_WORKSPACE";
+  }
+  return "UQ_ERR_UNKNOWN";
+}
+
+const char* uq_version(void) { return "uq 0.1 sm_100a"; }
+
+int32_t uq_last_launches(void) { return g_launches; }
+
+uq_status uq_timing_enable(int32_t on) {
+  g_timer.on = on != 0;
+  return UQ_OK;
+}
+
+uq_status uq_timing_collect(double* scan_ms, int64_t* launches) {
+  if (!scan_ms || !launches) return UQ_ERR_INVALID_ARG;
+  double tot = 0.0;
+  for (size_t i = 0; i < g_timer.used; ++i) {
+    auto& p = g_timer.ev[i];
+    if (cudaEventSynchronize(p.second) != cudaSuccess) return UQ_ERR_CUDA;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.first, p.second) != cudaSuccess) return UQ_ERR_CUDA;
+    tot += ms;
+  }
+  *scan_ms = tot;
+  *launches = (int64_t)g_timer.used;
+  g_timer.used = 0;
+  return UQ_OK;
+}
+
+uq_status uq_encode(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld_elems, int32_t x,
+                    uint8_t* codes, uq_stream_t stream) {
+  g_launches = 0;
+  if (n < 0 || d < 1 || x < 1 || x > d || ld_elems < d) return UQ_ERR_INVALID_ARG;
+  if (dt != UQ_F32 && dt != UQ_F16 && dt != UQ_BF16) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D) return UQ_ERR_UNSUPPORTED;
+  if (n == 0) return UQ_OK;
+  if (u == nullptr || codes == nullptr) return UQ_ERR_INVALID_ARG;
+  const size_t es = (dt == UQ_F32) ? 4 : 2;
+  if (((uintptr_t)u % es) != 0 || !aligned16(codes)) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_encode(u, dt, n, d, ld_elems, x, codes, device_sms(), (cudaStream_t)stream));
+}
+
+uq_status uq_scores(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                    int32_t* out, uq_stream_t stream) {
+  g_launches = 0;
+  if (nq < 0 || n < 0 || d < 1) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D) return UQ_ERR_UNSUPPORTED;
+  if (nq == 0 || n == 0) return UQ_OK;
+  if (!qcodes || !dbcodes || !out || !aligned16(qcodes) || !aligned16(dbcodes)) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_scores(qcodes, nq, dbcodes, n, d, out, (cudaStream_t)stream));
+}
+
+uq_status uq_search_workspace_ex(int64_t nq, int64_t n, int32_t d, int32_t k, uq_algo algo,
+                                 size_t* bytes) {
+  if (!bytes) return UQ_ERR_INVALID_ARG;
+  if (nq < 0 || n < 0 || d < 1 || k < 1) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D || k > UQ_MAX_K || n >= (int64_t)0xffffffffLL) return UQ_ERR_UNSUPPORTED;
+  const int sms = device_sms();
+  const uq_algo a = resolve_algo(algo, nq, n, d, k, sms);
+  if (a == UQ_ALGO_AUTO) return UQ_ERR_UNSUPPORTED;
+  *bytes = workspace_for(a, nq, n, d, k, sms);
+  return UQ_OK;
+}
+
+uq_status uq_search_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes) {
+  return uq_search_workspace_ex(nq, n, d, k, UQ_ALGO_AUTO, bytes);
+}
+
+uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                       int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
+                       void* workspace, size_t workspace_bytes, uq_algo algo, uq_stream_t stream) {
+  g_launches = 0;
+  uq_status s = validate_search(qcodes, nq, dbcodes, n, d, k);
+  if (s != UQ_OK) return s;
+  if (nq == 0) return UQ_OK;
+  if (!out_scores || !out_ids) return UQ_ERR_INVALID_ARG;
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int sms = device_sms();
+  if (n == 0) {  // nothing to scan: every row is padding
+    return from_cuda(launch_merge_keys(nullptr, 0, nq, k, k, id_base, out_scores, out_ids, st));
+  }
+  const uq_algo a = resolve_algo(algo, nq, n, d, k, sms);
+  if (a == UQ_ALGO_AUTO) return UQ_ERR_UNSUPPORTED;
+  const size_t need = workspace_for(a, nq, n, d, k, sms);
+  if (workspace_bytes < need || (need > 0 && workspace == nullptr)) return UQ_ERR_WORKSPACE;
+  if (((uintptr_t)workspace & 255u) != 0) return UQ_ERR_INVALID_ARG;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  if (a == UQ_ALGO_TCGEN05) {
+    const TcPlan tp = plan_tc(nq, n, d, k, sms);
+    uint32_t* bufs = reinterpret_cast<uint32_t*>(ws);
+    uint64_t* part = reinterpret_cast<uint64_t*>(ws + align_up(tp.buf_bytes, 256));
+    cudaEvent_t ev;
+    timer_begin(st, &ev);
+    cudaError_t e = launch_scan_tc(qcodes, nq, dbcodes, n, d, k, tp, bufs, part, st);
+    timer_end(st, ev);
+    if (e != cudaSuccess) return UQ_ERR_CUDA;
+    return from_cuda(launch_merge_keys(part, tp.n_chunks, nq, k, k, id_base, out_scores, out_ids, st));
+  }
+  const PopcPlan pl = plan_popc(nq, n, d, k, sms);
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(ws);
+  uint64_t* part = reinterpret_cast<uint64_t*>(ws + align_up(pl.buf_bytes, 256));
+  cudaEvent_t ev;
+  timer_begin(st, &ev);
+  cudaError_t e = launch_scan_popc(qcodes, nq, dbcodes, n, d, k, pl, bufs, part, st);
+  timer_end(st, ev);
+  if (e != cudaSuccess) return UQ_ERR_CUDA;
+  return from_cuda(launch_merge_keys(part, pl.n_chunks, nq, k, k, id_base, out_scores, out_ids, st));
+}
+
+uq_status uq_search(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                    int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids, void* workspace,
+                    size_t workspace_bytes, uq_stream_t stream) {
+  return uq_search_ex(qcodes, nq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace,
+                      workspace_bytes, UQ_ALGO_AUTO, stream);
+}
+
+uq_status uq_merge_topk(const int32_t* scores, const int64_t* ids, int32_t g, int64_t nq, int32_t k,
+                        int32_t* out_scores, int64_t* out_ids, uq_stream_t stream) {
+  g_launches = 0;
+  if (g < 0 || nq < 0 || k < 1) return UQ_ERR_INVALID_ARG;
+  if (k > UQ_MAX_K) return UQ_ERR_UNSUPPORTED;
+  if (nq == 0) return UQ_OK;
+  if (!out_scores || !out_ids || (g > 0 && (!scores || !ids))) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_merge_si(scores, ids, g, nq, k, out_scores, out_ids, (cudaStream_t)stream));
+}
+
+uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad_rows,
+                         uq_stream_t stream) {
+  g_launches = 0;
+  if (n < 0 || d < 1 || !bad_rows) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D) return UQ_ERR_UNSUPPORTED;
+  if (n > 0 && (!codes || !aligned16(codes))) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_check_codes(codes, n, d, bad_rows, device_sms(), (cudaStream_t)stream));
+}
+
+}  // extern "C"

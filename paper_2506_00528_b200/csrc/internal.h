@@ -1,0 +1,48 @@
+// internal.h -- launch plans and launchers shared between the C-ABI layer
+// (api.cu) and the kernel translation units.  Product path only.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/uq.h"
+
+namespace uq {
+
+void note_launch(int n = 1);
+
+cudaError_t launch_encode(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld, int32_t x,
+                          uint8_t* codes, int sms, cudaStream_t st);
+cudaError_t launch_scores(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                          int32_t* out, cudaStream_t st);
+cudaError_t launch_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad,
+                               int sms, cudaStream_t st);
+cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
+                              int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st);
+cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
+                            int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st);
+
+// Popcount scan (scan_popc.cu).
+struct PopcPlan {
+  int32_t qt, n_qtiles, cap, grid, smem;
+  int64_t L, n_chunks;
+  size_t buf_bytes, part_bytes;
+};
+PopcPlan plan_popc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                             int32_t k, const PopcPlan& pl, uint32_t* bufs, uint64_t* part,
+                             cudaStream_t st);
+
+// Tensor-core scan (scan_tc.cu).
+struct TcPlan {
+  bool ok;
+  int32_t grid, smem, n_qtiles, cap;
+  int64_t L, n_chunks;
+  size_t buf_bytes, part_bytes;
+};
+TcPlan plan_tc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                           int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
+                           cudaStream_t st);
+
+}  // namespace uq

@@ -18,3 +18,10 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_sessionstart(session):
+    # libuq.so is an in-tree build artefact (nvcc cross-compiles without a GPU);
+    # make sure it exists and is current before tests import the package.
+    import __graft_entry__
+    __graft_entry__.build_lib()

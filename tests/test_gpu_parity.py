@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element, on the same seeded inputs.  Integer / index outputs: bit-exact.
+
+Sizes span several tiles plus ragged tails; full BASELINE sizes are checked on
+sampled outputs (test_full_size_*).
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ("popc", "tc")
+
+
+@pytest.fixture(scope="module")
+def uq():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+    __graft_entry__.build_lib()
+    import paper_2506_00528_b200 as m
+    return m
+
+
+def _algo(uq, name):
+    return {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "auto": uq.ALGO_AUTO}[name]
+
+
+def _tc_supported(uq, nq, n, d, k):
+    try:
+        uq.search_workspace(nq, n, d, k, uq.ALGO_TCGEN05)
+        return True
+    except uq.UQError:
+        return False
+
+
+def _tie_heavy(rng, n, d, dtype=np.float32):
+    """Values on a small grid: many exact |u| ties, zeros and -0.0 (encoder stress)."""
+    u = rng.integers(-6, 7, size=(n, d)).astype(np.float32) / 8.0
+    u[rng.random((n, d)) < 0.02] = -0.0
+    return u.astype(dtype)
+
+
+# --------------------------------------------------------------------------
+# Encoder + pack
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("d", [1, 7, 10, 100, 128, 129, 300, 384, 768, 1000, 1024, 1536, 2048])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16, torch.bfloat16])
+def test_encode_parity_shapes(uq, orc, d, dt):
+    rng = np.random.default_rng(d * 7 + 1)
+    n = 777
+    u = rng.standard_normal((n, d)).astype(np.float32)
+    u[: n // 3] = _tie_heavy(rng, n // 3, d)
+    ut = torch.from_numpy(u).to(dt)
+    host = ut.float().numpy() if dt == torch.bfloat16 else ut.numpy()
+    for x in sorted({1, max(1, d // 3), max(1, d // 2), max(1, (2 * d) // 3), d}):
+        got = uq.encode(ut.cuda(), x).cpu().numpy()
+        ref = orc.pack(orc.encode(host, x))
+        assert np.array_equal(got, ref), (d, dt, x, np.argwhere((got != ref).any(1))[:5])
+
+
+def test_encode_strided_and_table3(uq, orc):
+    import json, os
+    t = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table3_p356.json")))
+    u = torch.tensor([t["u1"], t["u2"]], dtype=torch.float32)
+    got = uq.encode(u.cuda(), 5).cpu().numpy()
+    assert np.array_equal(got, orc.pack(orc.encode(u.numpy(), 5)))
+    assert got[0, 0] == 0x63 and got[0, 16] == 0x04          # v1+ / v1- of P:369-370
+    # row stride > d (ld_elems), unaligned row starts -> scalar-load path
+    rng = np.random.default_rng(0)
+    big = torch.from_numpy(rng.standard_normal((300, 401)).astype(np.float32)).cuda()
+    for view in (big[:, :384], big[:, 1:385], big[:, 3:300]):
+        d = view.shape[1]
+        got = uq.encode(view, d // 2).cpu().numpy()
+        ref = orc.pack(orc.encode(view.cpu().numpy(), d // 2))
+        assert np.array_equal(got, ref)
+
+
+def test_encode_c5_fp16_unnormalised(uq, orc):
+    """Config 5 recipe (fp16, raw mixture values; ~10% of rows tie at the top-x boundary)."""
+    w = datagen.CONFIGS["c5"].scaled(n=20000, nq=16)
+    u = datagen.db(w, "cuda")
+    got = uq.encode(u, w.x).cpu().numpy()
+    ref = orc.pack(orc.encode(u.cpu().numpy(), w.x))
+    assert np.array_equal(got, ref)
+
+
+# --------------------------------------------------------------------------
+# Dense Delta
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("d", [10, 384, 1000])
+def test_scores_parity(uq, orc, d):
+    rng = np.random.default_rng(d)
+    u = rng.standard_normal((1100, d)).astype(np.float32)
+    codes = uq.encode(torch.from_numpy(u).cuda(), max(1, d // 2))
+    q, db = codes[:60], codes[60:]
+    got = uq.scores(q, db, d).cpu().numpy()
+    ref = orc.scores(q.cpu().numpy(), db.cpu().numpy(), d)
+    assert np.array_equal(got, ref)
+
+
+# --------------------------------------------------------------------------
+# Search: scan + fused top-k + merge, every engine, ragged shapes, ties
+# --------------------------------------------------------------------------
+def _search_case(uq, orc, algo, d, x, n, nq, k, seed=0, mode="normal"):
+    rng = np.random.default_rng(seed)
+    if mode == "dup":
+        base = rng.standard_normal((max(1, n // 7), d)).astype(np.float32)
+        u_db = base[rng.integers(0, base.shape[0], size=n)]
+    elif mode == "ties":
+        u_db = _tie_heavy(rng, n, d)
+    else:
+        u_db = rng.standard_normal((n, d)).astype(np.float32)
+    u_q = rng.standard_normal((nq, d)).astype(np.float32)
+    if n > 0 and nq > 1:
+        u_q[0] = u_db[n // 2]   # a stored vector as query: self-match first
+    o_db = orc.pack(orc.encode(u_db, x)) if n else np.zeros((0, 2 * orc.plane_bytes(d)), np.uint8)
+    o_q = orc.pack(orc.encode(u_q, x))
+    a = _algo(uq, algo)
+    if algo == "tc" and not _tc_supported(uq, nq, n, d, k):
+        pytest.skip("tcgen05 path does not support this shape")
+    s, i = uq.search(torch.from_numpy(o_q).cuda(), torch.from_numpy(o_db).cuda(), d, k,
+                     id_base=5, algo=a)
+    s_ref, i_ref = orc.knn(o_q, o_db, d, k, id_base=5)
+    s, i = s.cpu().numpy(), i.cpu().numpy()
+    assert np.array_equal(s, s_ref), (algo, d, n, nq, k, np.argwhere(s != s_ref)[:5])
+    assert np.array_equal(i, i_ref), (algo, d, n, nq, k, np.argwhere(i != i_ref)[:5])
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("n,nq,k", [(0, 3, 4), (1, 2, 1), (9, 4, 10), (255, 1, 10), (257, 65, 10),
+                                    (1000, 100, 100), (5000, 130, 10), (3000, 7, 1024),
+                                    (20000, 200, 100), (70000, 3, 10)])
+def test_search_parity_shapes(uq, orc, algo, n, nq, k):
+    _search_case(uq, orc, algo, 384, 192, n, nq, k, seed=n + nq + k)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("d,x", [(10, 5), (100, 67), (768, 384), (1000, 667), (1024, 256),
+                                 (1536, 768), (2048, 1024), (129, 1)])
+def test_search_parity_dims(uq, orc, algo, d, x):
+    _search_case(uq, orc, algo, d, x, 6000, 150, 10, seed=d)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mode", ["dup", "ties"])
+def test_search_parity_ties(uq, orc, algo, mode):
+    """Duplicated rows / grid-valued inputs: massive Delta ties -> order decided by id."""
+    _search_case(uq, orc, algo, 256, 128, 9000, 140, 50, seed=3, mode=mode)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_search_c1_full(uq, orc, algo):
+    """BASELINE config 1 at full size (N=10,000, Q=100, d=384, x=192, k=10)."""
+    w = datagen.CONFIGS["c1"]
+    db = datagen.db(w, "cuda")
+    q = datagen.queries(w, "cuda")
+    dbc, qc = uq.encode(db, w.x), uq.encode(q, w.x)
+    o_db = orc.pack(orc.encode(db.cpu().numpy(), w.x))
+    o_q = orc.pack(orc.encode(q.cpu().numpy(), w.x))
+    assert np.array_equal(dbc.cpu().numpy(), o_db) and np.array_equal(qc.cpu().numpy(), o_q)
+    assert np.array_equal(uq.scores(qc, dbc, w.d).cpu().numpy(), orc.scores(o_q, o_db, w.d))
+    if algo == "tc" and not _tc_supported(uq, w.nq, w.n, w.d, w.k):
+        pytest.skip("tcgen05 path does not support this shape")
+    s, i = uq.search(qc, dbc, w.d, w.k, algo=_algo(uq, algo))
+    s_ref, i_ref = orc.knn(o_q, o_db, w.d, w.k)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
+
+
+def test_full_size_c2_sampled(uq, orc):
+    """Config 2 at full size in the bench launch shape (N=1e6, Q=1000, k=100, AUTO):
+    codes checked on a seeded 2^14-row sample; top-k of 6 seeded queries checked
+    against the oracle's exhaustive kNN over all 10^6 oracle-encoded rows."""
+    w = datagen.CONFIGS["c2"]
+    db = datagen.db(w, "cuda")
+    q = datagen.queries(w, "cuda")
+    dbc, qc = uq.encode(db, w.x), uq.encode(q, w.x)
+    s, i = uq.search(qc, dbc, w.d, w.k)              # whole batch, as bench.py runs it
+    db_h = db.cpu().numpy()
+    del db
+    o_db = orc.pack(orc.encode(db_h, w.x))
+    rng = np.random.default_rng(2)
+    rows = rng.choice(w.n, size=1 << 14, replace=False)
+    assert np.array_equal(dbc[torch.from_numpy(rows).cuda()].cpu().numpy(), o_db[rows])
+    qs = np.sort(rng.choice(w.nq, size=6, replace=False))
+    o_q = orc.pack(orc.encode(q.cpu().numpy()[qs], w.x))
+    assert np.array_equal(qc.cpu().numpy()[qs], o_q)
+    s_ref, i_ref = orc.knn(o_q, o_db, w.d, w.k)
+    assert np.array_equal(s.cpu().numpy()[qs], s_ref)
+    assert np.array_equal(i.cpu().numpy()[qs], i_ref)
+
+
+# --------------------------------------------------------------------------
+# Merge (multi-GPU exchange step) and sharding invariance
+# --------------------------------------------------------------------------
+def test_merge_topk_parity(uq, orc):
+    rng = np.random.default_rng(8)
+    g, nq, k = 5, 33, 17
+    sc = rng.integers(-20, 21, size=(g, nq, k)).astype(np.int32)
+    ids = np.empty((g, nq, k), np.int64)
+    for q in range(nq):
+        ids[:, q, :] = rng.permutation(10 * g * k)[: g * k].reshape(g, k)
+    ids[1, :, 10:] = -1                       # padding entries
+    sc[1, :, 10:] = np.iinfo(np.int32).min
+    s, i = uq.merge_topk(torch.from_numpy(sc).cuda(), torch.from_numpy(ids).cuda(), k)
+    for q in range(nq):
+        cand = [(int(sc[a, q, b]), int(ids[a, q, b])) for a in range(g) for b in range(k)
+                if ids[a, q, b] >= 0]
+        cand.sort(key=lambda t: (-t[0], t[1]))
+        assert s[q].cpu().tolist() == [c[0] for c in cand[:k]]
+        assert i[q].cpu().tolist() == [c[1] for c in cand[:k]]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_sharded_equals_unsharded(uq, orc, algo, G):
+    """Shard -> local search with id_base -> merge == unsharded search (R8)."""
+    rng = np.random.default_rng(G)
+    d, x, n, nq, k = 768, 384, 20000, 96, 100
+    u = torch.from_numpy(rng.standard_normal((n + nq, d)).astype(np.float32)).cuda()
+    codes = uq.encode(u, x)
+    db, q = codes[:n], codes[n:]
+    a = _algo(uq, algo)
+    if algo == "tc" and not _tc_supported(uq, nq, n // G, d, k):
+        pytest.skip("tcgen05 path does not support this shape")
+    s0, i0 = uq.search(q, db, d, k, algo=a)
+    bounds = np.linspace(0, n, G + 1).astype(int)
+    parts = [uq.search(q, db[bounds[j]:bounds[j + 1]], d, k, id_base=int(bounds[j]), algo=a)
+             for j in range(G)]
+    s, i = uq.merge_topk(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]), k)
+    assert torch.equal(s, s0) and torch.equal(i, i0)
+    o = orc.knn(q.cpu().numpy(), db.cpu().numpy(), d, k)
+    assert np.array_equal(s0.cpu().numpy(), o[0]) and np.array_equal(i0.cpu().numpy(), o[1])
+
+
+def test_check_codes_parity(uq, orc):
+    rng = np.random.default_rng(4)
+    d = 300
+    codes = uq.encode(torch.from_numpy(rng.standard_normal((500, d)).astype(np.float32)).cuda(), 100)
+    assert uq.check_codes(codes, d) == 0
+    h = codes.cpu().numpy()
+    pb = h.shape[1] // 2
+    h[3, 0] |= 1; h[3, pb] |= 1
+    h[9, pb - 1] |= 0x80           # pos-plane pad bit 383 >= d
+    h[10, 2 * pb - 2] |= 0x01      # neg-plane pad bit 368 >= d
+    assert uq.check_codes(torch.from_numpy(h).cuda(), d) == orc.check_codes(h, d) == 3
+
+
+def test_errors_are_loud(uq):
+    with pytest.raises(uq.UQError):
+        uq.encode(torch.zeros(4, 16, device="cuda"), 0)
+    with pytest.raises(ValueError):
+        uq.encode(torch.zeros(4, 16), 4)          # CPU tensor: no CPU path
