@@ -302,7 +302,7 @@ def main():
     peaks, peaks_src = _peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    used_tc = (algo == uq.ALGO_TCGEN05) or (algo == uq.ALGO_AUTO and _auto_is_tc(uq, nq, n_loc, d, k))
+    used_tc = uq.search_resolve(nq, n_loc, d, k, algo) == uq.ALGO_TCGEN05
     scan_avg_s = (scan_ms / max(scan_n, 1)) * 1e-3
     if used_tc:
         # int8 MACs: d per Delta (the int8 GEMM T_q . T_db^T), 2 ops per MAC
@@ -354,13 +354,6 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
-
-
-def _auto_is_tc(uq, nq, n, d, k):
-    try:
-        return uq.search_workspace(nq, n, d, k, uq.ALGO_TCGEN05) > 0 and nq >= 64
-    except uq.UQError:
-        return False
 
 
 if __name__ == "__main__":

@@ -99,6 +99,14 @@ uq_status uq_search_workspace_ex(int64_t nq, int64_t n, int32_t d, int32_t k, uq
                                  size_t* bytes);
 
 /*
+ * uq_search_resolve -- which scan engine uq_search_ex(algo) runs for this shape
+ * on the CURRENT device (*resolved is a host pointer; UQ_ALGO_POPC or
+ * UQ_ALGO_TCGEN05).  UQ_ERR_UNSUPPORTED if `algo` cannot run this shape.
+ */
+uq_status uq_search_resolve(int64_t nq, int64_t n, int32_t d, int32_t k, uq_algo algo,
+                            uq_algo* resolved);
+
+/*
  * uq_search -- exhaustive kNN in the proxy space (P:61 problem statement;
  * P:480 "exhaustive queries over the whole data").  For every query q: Delta
  * against every row r of dbcodes, keep the k best under (Delta desc, id asc),

@@ -16,7 +16,7 @@ import torch
 
 __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
-    "search_workspace", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05",
+    "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05",
     "last_launches", "version", "timing_enable", "timing_collect",
 ]
 
@@ -51,9 +51,10 @@ def _load():
     L.uq_search_ex.argtypes = [vp, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, i32, vp]
     L.uq_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
     L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
+    L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
     L.uq_timing_enable.argtypes = [i32]
     L.uq_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
-    for f in ("uq_timing_enable", "uq_timing_collect", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
+    for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
               "uq_check_codes"):
         getattr(L, f).restype = i32
     return L
@@ -144,6 +145,13 @@ def search_workspace(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> 
     b = ctypes.c_size_t(0)
     _check("uq_search_workspace", _L.uq_search_workspace_ex(nq, n, d, k, algo, ctypes.byref(b)))
     return int(b.value)
+
+
+def search_resolve(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> int:
+    """Scan engine (ALGO_POPC / ALGO_TCGEN05) that search(algo) runs for this shape."""
+    r = ctypes.c_int32(0)
+    _check("uq_search_resolve", _L.uq_search_resolve(nq, n, d, k, algo, ctypes.byref(r)))
+    return int(r.value)
 
 
 def search(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base: int = 0,

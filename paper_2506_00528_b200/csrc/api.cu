@@ -60,10 +60,17 @@ static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; 
 
 static uq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? UQ_OK : UQ_ERR_CUDA; }
 
+// The tensor-core engine runs on CTA pairs (cta_group::2) once the query
+// batch fills a 256-query pair tile; smaller batches use the one-CTA kernel.
+static bool use_pairs(int64_t nq) { return nq > 128; }
+static TcPlan plan_tc_any(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  return use_pairs(nq) ? plan_tc2(nq, n, d, k, sms) : plan_tc(nq, n, d, k, sms);
+}
+
 // Which scan engine runs for a shape.
 static uq_algo resolve_algo(uq_algo algo, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   if (algo == UQ_ALGO_POPC) return UQ_ALGO_POPC;
-  const TcPlan tp = plan_tc(nq, n, d, k, sms);
+  const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
   if (algo == UQ_ALGO_TCGEN05) return tp.ok ? UQ_ALGO_TCGEN05 : UQ_ALGO_AUTO /* unsupported */;
   // AUTO: the popcount scan is POPC-issue-bound once nq exceeds ~3 (DESIGN.md
   // roofline); the int8 tensor path wins for query batches that fill an M tile.
@@ -81,14 +88,89 @@ static uq_status validate_search(const uint8_t* q, int64_t nq, const uint8_t* db
   return UQ_OK;
 }
 
-static size_t workspace_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  if (nq == 0 || n == 0) return 0;
+// ---- threshold seeding ----------------------------------------------------
+// A first scan over a strided sample of the database (every stride-th row)
+// yields, per query, the k-th best Delta of the sample, D_k.  At least k rows
+// then have Delta >= D_k, so a row with Delta < D_k can never be in the top-k:
+// the main scan starts every query's stream at "pass iff Delta > D_k - 1"
+// instead of "pass everything".  Exact by construction; it only removes
+// candidates that the final selection would have discarded.
+struct SeedPlan {
+  bool on;
+  int64_t rows, stride;
+};
+static SeedPlan plan_seed(int64_t n, int32_t k) {
+  SeedPlan sp{false, 0, 1};
+  if (n < (int64_t)1 << 16) return sp;
+  int64_t rows = n / 32;
+  if (rows < 16 * (int64_t)k) return sp;
+  sp.on = true;
+  sp.stride = n / rows;
+  sp.rows = n / sp.stride;
+  return sp;
+}
+
+struct SearchLayout {
+  size_t bufs_off, part_off, seed_s_off, seed_i_off, total;
+};
+
+static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms,
+                           size_t* buf_bytes) {
   if (a == UQ_ALGO_TCGEN05) {
-    const TcPlan tp = plan_tc(nq, n, d, k, sms);
-    return align_up(tp.buf_bytes, 256) + align_up(tp.part_bytes, 256);
+    const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
+    *buf_bytes = align_up(tp.buf_bytes, 256);
+    return align_up(tp.part_bytes, 256);
   }
   const PopcPlan pl = plan_popc(nq, n, d, k, sms);
-  return align_up(pl.buf_bytes, 256) + align_up(pl.part_bytes, 256);
+  *buf_bytes = align_up(pl.buf_bytes, 256);
+  return align_up(pl.part_bytes, 256);
+}
+
+static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  SearchLayout L{0, 0, 0, 0, 0};
+  if (nq == 0 || n == 0) return L;
+  size_t bufs = 0, part = engine_bytes(a, nq, n, d, k, sms, &bufs);
+  const SeedPlan sp = plan_seed(n, k);
+  if (sp.on) {
+    size_t b2 = 0, p2 = engine_bytes(a, nq, sp.rows, d, k, sms, &b2);
+    if (b2 > bufs) bufs = b2;
+    if (p2 > part) part = p2;
+  }
+  L.bufs_off = 0;
+  L.part_off = bufs;
+  L.seed_s_off = L.part_off + part;
+  L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * k * 4, 256) : 0);
+  L.total = L.seed_i_off + (sp.on ? align_up((size_t)nq * k * 8, 256) : 0);
+  return L;
+}
+
+static size_t workspace_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  return layout_for(a, nq, n, d, k, sms).total;
+}
+
+// One scan (+ merge) of rows {i * row_stride : i < n} into out_scores / out_ids.
+static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n,
+                                  int32_t d, int32_t k, int64_t id_base, int64_t row_stride,
+                                  const int32_t* thr0, int32_t thr0_stride, uint32_t* bufs,
+                                  uint64_t* part, int32_t* out_s, int64_t* out_id, int sms,
+                                  cudaStream_t st) {
+  cudaEvent_t ev;
+  int64_t lists = 0;
+  cudaError_t e;
+  timer_begin(st, &ev);
+  if (a == UQ_ALGO_TCGEN05) {
+    const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
+    e = use_pairs(nq) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st)
+                      : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
+    lists = tp.n_chunks;
+  } else {
+    const PopcPlan pl = plan_popc(nq, n, d, k, sms);
+    e = launch_scan_popc(q, nq, db, n, d, k, pl, bufs, part, thr0, thr0_stride, row_stride, st);
+    lists = pl.n_chunks;
+  }
+  timer_end(st, ev);
+  if (e != cudaSuccess) return e;
+  return launch_merge_keys(part, lists, nq, k, k, id_base, out_s, out_id, st);
 }
 
 }  // namespace uq
@@ -170,6 +252,17 @@ uq_status uq_search_workspace_ex(int64_t nq, int64_t n, int32_t d, int32_t k, uq
   return UQ_OK;
 }
 
+uq_status uq_search_resolve(int64_t nq, int64_t n, int32_t d, int32_t k, uq_algo algo,
+                            uq_algo* resolved) {
+  if (!resolved) return UQ_ERR_INVALID_ARG;
+  if (nq < 0 || n < 0 || d < 1 || k < 1) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D || k > UQ_MAX_K || n >= (int64_t)0xffffffffLL) return UQ_ERR_UNSUPPORTED;
+  const uq_algo a = resolve_algo(algo, nq, n, d, k, device_sms());
+  if (a == UQ_ALGO_AUTO) return UQ_ERR_UNSUPPORTED;
+  *resolved = a;
+  return UQ_OK;
+}
+
 uq_status uq_search_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes) {
   return uq_search_workspace_ex(nq, n, d, k, UQ_ALGO_AUTO, bytes);
 }
@@ -193,26 +286,23 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   if (workspace_bytes < need || (need > 0 && workspace == nullptr)) return UQ_ERR_WORKSPACE;
   if (((uintptr_t)workspace & 255u) != 0) return UQ_ERR_INVALID_ARG;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  if (a == UQ_ALGO_TCGEN05) {
-    const TcPlan tp = plan_tc(nq, n, d, k, sms);
-    uint32_t* bufs = reinterpret_cast<uint32_t*>(ws);
-    uint64_t* part = reinterpret_cast<uint64_t*>(ws + align_up(tp.buf_bytes, 256));
-    cudaEvent_t ev;
-    timer_begin(st, &ev);
-    cudaError_t e = launch_scan_tc(qcodes, nq, dbcodes, n, d, k, tp, bufs, part, st);
-    timer_end(st, ev);
+  const SearchLayout L = layout_for(a, nq, n, d, k, sms);
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(ws + L.bufs_off);
+  uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part_off);
+  const SeedPlan sp = plan_seed(n, k);
+  const int32_t* thr0 = nullptr;
+  if (sp.on) {
+    int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
+    int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
+    cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, sp.rows, d, k, 0, sp.stride, nullptr, 0,
+                                   bufs, part, seed_s, seed_i, sms, st);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
-    return from_cuda(launch_merge_keys(part, tp.n_chunks, nq, k, k, id_base, out_scores, out_ids, st));
+    thr0 = seed_s + (k - 1);  // k-th best sample Delta, row stride k
   }
-  const PopcPlan pl = plan_popc(nq, n, d, k, sms);
-  uint32_t* bufs = reinterpret_cast<uint32_t*>(ws);
-  uint64_t* part = reinterpret_cast<uint64_t*>(ws + align_up(pl.buf_bytes, 256));
-  cudaEvent_t ev;
-  timer_begin(st, &ev);
-  cudaError_t e = launch_scan_popc(qcodes, nq, dbcodes, n, d, k, pl, bufs, part, st);
-  timer_end(st, ev);
-  if (e != cudaSuccess) return UQ_ERR_CUDA;
-  return from_cuda(launch_merge_keys(part, pl.n_chunks, nq, k, k, id_base, out_scores, out_ids, st));
+  // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
+  cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, k, bufs, part,
+                                 out_scores, out_ids, sms, st);
+  return from_cuda(e);
 }
 
 uq_status uq_search(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,

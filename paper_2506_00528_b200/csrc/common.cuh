@@ -76,51 +76,124 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // ---------------------------------------------------------------------------
 // Warp-cooperative "stream" selector.  A stream is a candidate buffer of
-// 32-bit local keys in global memory plus a threshold `thr`: a new key enters
-// only if key > thr, where thr is the k-th largest key retained so far (0
-// while fewer than k keys exist).  A key <= thr can never reach the stream's
-// final top-k because k distinct larger keys are already retained.
+// 32-bit local keys in global memory plus a threshold: a new key enters only
+// if it beats the k-th best key retained so far (everything while fewer than
+// k are retained).  A key that does not can never reach the stream's final
+// top-k, because k distinct better keys already exist.
 //
-// rebuild(): the whole warp (all 32 lanes, converged) finds T = k-th largest
-// of the cnt buffered keys by bisection over the 32 key bits, then compacts the
-// keys >= T (exactly k of them: keys are unique) to the buffer front.  Returns
-// the new threshold; the new count is min(cnt, k).
+// A rebuild cuts a buffer of cnt > k keys back to exactly its k best.  The
+// whole warp cooperates (all 32 lanes converged); the keys are loaded into
+// registers once (lane l holds buffer entries l, l+32, ...), so the selection
+// costs no memory round trips beyond one load and one store per key.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t warp_count_ge(const uint32_t* buf, int cnt, uint32_t t, int lane) {
-  int c = 0;
-  for (int i = lane; i < cnt; i += kWarp) c += (buf[i] >= t) ? 1 : 0;
-  return __reduce_add_sync(kFull, (unsigned)c);
+template <int MAXR>
+__device__ __forceinline__ void stream_load(const uint32_t* buf, int cnt, int lane, uint32_t (&r)[MAXR]) {
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) {
+    const int idx = i * kWarp + lane;
+    r[i] = (idx < cnt) ? buf[idx] : 0u;
+  }
 }
 
-__device__ inline uint32_t stream_rebuild(uint32_t* buf, int cnt, int k, int lane) {
-  if (cnt <= k) return 0u;  // fewer than k candidates: keep all, accept everything
+// General stream (keys appended in any row order): T = k-th largest key by
+// bisection over the 32 key bits; keep the keys >= T (exactly k: keys are
+// unique).  Returns the smallest retained key (the new threshold: pass iff
+// key > thr).
+template <int MAXR>
+__device__ uint32_t stream_rebuild_regs(uint32_t* buf, int cnt, int k, int lane) {
+  uint32_t r[MAXR];
+  stream_load<MAXR>(buf, cnt, lane, r);
   uint32_t T = 0;
+#pragma unroll 1
   for (int b = 31; b >= 0; --b) {
-    uint32_t cand = T | (1u << b);
-    uint32_t c = warp_count_ge(buf, cnt, cand, lane);
-    if (c >= (uint32_t)k) {
+    const uint32_t cand = T | (1u << b);
+    unsigned c = 0;
+#pragma unroll
+    for (int i = 0; i < MAXR; ++i) c += (r[i] >= cand) ? 1u : 0u;
+    const unsigned tot = __reduce_add_sync(kFull, c);
+    if (tot >= (unsigned)k) {
       T = cand;
-      if (c == (uint32_t)k) break;  // exactly k keys >= cand: cand is a valid cut
+      if (tot == (unsigned)k) break;  // exactly k keys >= cand: a valid cut
     }
   }
-  // compact keys >= T to the front (write index <= read index: in-place safe)
   int w = 0;
   uint32_t kmin = 0xffffffffu;
-  for (int base = 0; base < cnt; base += kWarp) {
-    int i = base + lane;
-    uint32_t key = (i < cnt) ? buf[i] : 0u;
-    bool keep = (i < cnt) && key >= T;
-    unsigned bal = __ballot_sync(kFull, keep);
-    __syncwarp();
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) {
+    const bool keep = (i * kWarp + lane < cnt) && r[i] >= T;
+    const unsigned bal = __ballot_sync(kFull, keep);
     if (keep) {
-      buf[w + __popc(bal & lanemask_lt())] = key;
-      kmin = min(kmin, key);
+      buf[w + __popc(bal & lanemask_lt())] = r[i];
+      kmin = min(kmin, r[i]);
     }
     w += __popc(bal);
-    __syncwarp();
   }
-  // w == k here.  Threshold for future keys: the smallest retained key.
+  __syncwarp();
   return __reduce_min_sync(kFull, kmin);
+}
+
+// Ordered stream (one producer appending rows in increasing order, e.g. one
+// query per thread scanning its chunk front to back): the buffer order is the
+// row order, so among equal Delta the earlier entries win.  D = k-th largest
+// Delta field (key >> rb) by bisection over the sb field bits; keep every key
+// with field > D plus the first (k - #{field > D}) keys with field == D.
+// Returns D: later keys pass iff their field > D (equal Delta, larger row).
+template <int MAXR>
+__device__ uint32_t ordered_rebuild_regs(uint32_t* buf, int cnt, int k, int lane, int rb) {
+  uint32_t r[MAXR];
+  stream_load<MAXR>(buf, cnt, lane, r);
+  const int sb = 32 - rb;
+  uint32_t D = 0;
+#pragma unroll 1
+  for (int b = sb - 1; b >= 0; --b) {
+    const uint32_t cand = D | (1u << b);
+    unsigned c = 0;
+#pragma unroll
+    for (int i = 0; i < MAXR; ++i) c += ((r[i] >> rb) >= cand) ? 1u : 0u;
+    const unsigned tot = __reduce_add_sync(kFull, c);
+    if (tot >= (unsigned)k) {
+      D = cand;
+      if (tot == (unsigned)k) break;
+    }
+  }
+  unsigned gt = 0;
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) gt += ((r[i] >> rb) > D) ? 1u : 0u;
+  const int m = k - (int)__reduce_add_sync(kFull, gt);  // entries with field == D to keep
+  int w = 0, eq_seen = 0;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) {
+    const bool in = i * kWarp + lane < cnt;
+    const uint32_t f = r[i] >> rb;
+    const bool eq = in && f == D;
+    const unsigned beq = __ballot_sync(kFull, eq);
+    const bool keep = in && (f > D || (eq && eq_seen + __popc(beq & lanemask_lt()) < m));
+    eq_seen += __popc(beq);
+    const unsigned bal = __ballot_sync(kFull, keep);
+    if (keep) buf[w + __popc(bal & lanemask_lt())] = r[i];
+    w += __popc(bal);
+  }
+  __syncwarp();
+  return D;
+}
+
+#define UQ_REBUILD_DISPATCH(FN, ...)                          \
+  do {                                                        \
+    if (cnt <= 8 * kWarp) return FN<8>(__VA_ARGS__);          \
+    if (cnt <= 16 * kWarp) return FN<16>(__VA_ARGS__);        \
+    if (cnt <= 24 * kWarp) return FN<24>(__VA_ARGS__);        \
+    if (cnt <= 32 * kWarp) return FN<32>(__VA_ARGS__);        \
+    return FN<48>(__VA_ARGS__);                               \
+  } while (0)
+
+// cnt <= 48*32 = 1536 (= UQ_MAX_K + 2*256 buffer capacity)
+__device__ __forceinline__ uint32_t stream_rebuild(uint32_t* buf, int cnt, int k, int lane) {
+  UQ_REBUILD_DISPATCH(stream_rebuild_regs, buf, cnt, k, lane);
+}
+__device__ __forceinline__ uint32_t ordered_rebuild(uint32_t* buf, int cnt, int k, int lane, int rb) {
+  UQ_REBUILD_DISPATCH(ordered_rebuild_regs, buf, cnt, k, lane, rb);
 }
 
 }  // namespace uq

@@ -31,18 +31,29 @@ struct PopcPlan {
 PopcPlan plan_popc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
 cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                              int32_t k, const PopcPlan& pl, uint32_t* bufs, uint64_t* part,
+                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                              cudaStream_t st);
 
 // Tensor-core scan (scan_tc.cu).
 struct TcPlan {
   bool ok;
-  int32_t grid, smem, n_qtiles, cap;
-  int64_t L, n_chunks;
+  int32_t grid, smem, n_qtiles, cap, stages;
+  int32_t s_lo, r_hi;   // query tile t is split into s_lo + (t < r_hi) DB chunks
+  int64_t n_items;
+  int64_t n_chunks;     // lists per query for the merge (= max chunks per tile)
   size_t buf_bytes, part_bytes;
 };
 TcPlan plan_tc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
 cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
+                           const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                            cudaStream_t st);
+
+// Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128.
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
+                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
+                            cudaStream_t st);
 
 }  // namespace uq

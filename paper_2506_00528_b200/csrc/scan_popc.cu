@@ -41,6 +41,9 @@ struct PopcParams {
   int32_t cap;       // stream buffer capacity (k + 2*kStageRows)
   uint32_t* bufs;    // [gridDim.x][qt][cap]
   uint64_t* part;    // [S][nq][k] global keys
+  const int32_t* thr0;  // optional per-query seed D_k: rows with Delta < thr0[q * thr0_stride] cannot matter
+  int32_t thr0_stride;
+  int64_t row_stride;   // DB row r of this scan is row r * row_stride of dbcodes
 };
 
 template <int NB>
@@ -72,7 +75,15 @@ __global__ void __launch_bounds__(kScanThreads, (NB <= 10 ? 2 : 1)) scan_popc_ke
       s_qm[i] = make_uint4(a.x | b.x, a.y | b.y, a.z | b.z, a.w | b.w);
       s_qn[i] = b;
     }
-    for (int j = threadIdx.x; j < nqt; j += kScanThreads) { s_thr[j] = 0u; s_cnt[j] = 0; }
+    for (int j = threadIdx.x; j < nqt; j += kScanThreads) {
+      uint32_t t0 = 0u;  // key > t0  <=>  Delta >= D_k (t0 has all row bits set)
+      if (p.thr0) {
+        const int32_t dk = p.thr0[(q0 + j) * p.thr0_stride];
+        if (dk != INT32_MIN && dk - 1 + p.kf.off >= 0) t0 = ((uint32_t)(dk - 1 + p.kf.off) << p.kf.rb) | p.kf.rmask;
+      }
+      s_thr[j] = t0;
+      s_cnt[j] = 0;
+    }
     __syncthreads();
 
     for (int64_t s0 = 0; s0 < rows; s0 += kStageRows) {
@@ -81,7 +92,7 @@ __global__ void __launch_bounds__(kScanThreads, (NB <= 10 ? 2 : 1)) scan_popc_ke
       // dm = r+ | r- and dn = r- of this lane's row, in registers
       uint4 dm[NB], dn[NB];
       if (valid) {
-        const uint8_t* rr = p.db + (row0 + lr) * cb;
+        const uint8_t* rr = p.db + (row0 + lr) * p.row_stride * cb;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           const uint4 dp = __ldg(reinterpret_cast<const uint4*>(rr) + b);
@@ -177,9 +188,10 @@ static cudaError_t launch_popc_nb(const PopcParams& p, const PopcPlan& pl, cudaS
 
 cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                              int32_t k, const PopcPlan& pl, uint32_t* bufs, uint64_t* part,
+                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                              cudaStream_t st) {
   PopcParams p{q, nq, db, n, d, k, make_keyfmt(d), pl.qt, pl.n_qtiles, pl.n_chunks, pl.L, pl.cap,
-               bufs, part};
+               bufs, part, thr0, thr0_stride, row_stride};
   switch (blocks128(d)) {
 #define UQ_POPC_CASE(N) \
   case N: return launch_popc_nb<N>(p, pl, st);

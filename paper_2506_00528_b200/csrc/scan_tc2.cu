@@ -1,0 +1,442 @@
+// scan_tc2.cu -- Delta as an int8 GEMM on CTA pairs (tcgen05.mma.cta_group::2
+// .kind::i8 -> UTCIMMA.2CTA), fused with the per-query top-k.
+//
+// Same contraction as scan_tc.cu (Delta = T_q . T_db^T over {-1,0,1}, s32,
+// exact; P:209-216 / P:385-389) on a 2-CTA cluster: the pair computes a
+// 256-query x 192-row tile per K step.  CTA r of the pair
+//   * keeps its own 128 queries resident in SMEM (A, 128 x 128*NB int8),
+//   * expands only rows [96 r, 96 r + 96) of each 192-row DB tile (its half
+//     of B), so each SM expands half as many DB rows per unit of MMA work as
+//     the one-CTA kernel -- the expansion is the per-SM instruction bottleneck,
+//   * holds the 128 x 192 s32 accumulator of its own queries in TMEM (two
+//     buffers) and runs their top-k streams in its epilogue warps.
+// The leader CTA (rank 0) issues the MMAs; its `full` barriers count the
+// producer warps of both CTAs (the peer arrives through shared::cluster), the
+// MMA commits multicast to both CTAs' `empty` / `tfull` barriers, and both
+// CTAs' epilogue warps arrive on the leader's `tempty`.
+//
+// Warps: 0-2 producers (one thread per DB row of this CTA's 96-row half),
+// 3 MMA issuer (leader) + TMEM owner, 4-11 epilogue in two sets of four
+// (warp % 4 = TMEM lane quarter; set h reads accumulator columns
+// [96 h, 96 h + 96)).  N = 192 per pair tile.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tc_common.cuh"
+
+namespace uq {
+namespace tc2 {
+
+using namespace ::uq::tc;
+
+constexpr int BM = 128;               // queries per CTA (pair M = 256)
+constexpr int BN = 192;               // DB rows per pair tile (UMMA N)
+constexpr int BH = BN / 2;            // DB rows expanded per CTA (96: three producer warps)
+constexpr int KB = 128;               // K bytes (dims) per stage
+constexpr int kProdWarps = 3;         // warps 0-2
+constexpr int kMmaWarp = 3;           // warp 3: MMA issuer (leader) + TMEM owner
+constexpr int kEpiSets = 2;           // epilogue warp sets, each owns half of a tile's columns
+constexpr int kEpiWarp0 = 4;          // warps 4..11 (warp % 4 = TMEM lane quarter)
+constexpr int kThreads = (4 + 4 * kEpiSets) * 32;  // 12 warps: 3 per SMSP -> 168 regs
+constexpr int kAccStride = 256;       // TMEM column offset of the second accumulator
+constexpr int kStageBytes = BH * KB;  // 16 KB per CTA per stage
+constexpr uint32_t kTmemCols = 512;   // two s32 accumulators (columns 0 and 256)
+constexpr int kEpiStageWords = 4 * 2 * 32 * 32;  // epilogue staging: one 32-score row per thread
+
+struct Params {
+  const uint8_t* q;
+  int64_t nq;
+  const uint8_t* db;
+  int64_t n;
+  int32_t d;
+  int32_t k;
+  KeyFmt kf;
+  int32_t n_qtiles;     // pair tiles of 256 queries
+  int32_t s_lo, r_hi, s_max;
+  int64_t n_items;
+  int32_t cap;
+  int32_t stages;
+  uint32_t* bufs;       // [gridDim.x][kEpiSets*BM][cap]
+  uint64_t* part;       // [s_max*kEpiSets][nq][k]
+  const int32_t* thr0;  // optional per-query seed D_k (rows with Delta < D_k cannot matter)
+  int32_t thr0_stride;
+  int64_t row_stride;
+  int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads
+};
+
+struct Item {
+  int t, c, s_t;
+  int64_t row0, rows;
+};
+
+__device__ __forceinline__ Item decode_item(const Params& p, int64_t i) {
+  Item it;
+  const int64_t big = (int64_t)p.r_hi * (p.s_lo + 1);
+  if (i < big) {
+    it.t = (int)(i / (p.s_lo + 1));
+    it.c = (int)(i % (p.s_lo + 1));
+    it.s_t = p.s_lo + 1;
+  } else {
+    const int64_t j = i - big;
+    it.t = p.r_hi + (int)(j / p.s_lo);
+    it.c = (int)(j % p.s_lo);
+    it.s_t = p.s_lo;
+  }
+  int64_t L = (p.n + it.s_t - 1) / it.s_t;
+  L = (L + BN - 1) / BN * BN;
+  it.row0 = (int64_t)it.c * L;
+  it.rows = p.n - it.row0;
+  if (it.rows > L) it.rows = L;
+  if (it.rows < 0) it.rows = 0;
+  return it;
+}
+
+template <int NB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc2_kernel(Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int KTOT = NB * KB;
+  constexpr uint32_t A_LBO = BM * 16;   // next 16-B K chunk of A (128 rows)
+  constexpr uint32_t B_LBO = BH * 16;   // next 16-B K chunk of this CTA's B half
+  constexpr uint32_t SBO = 128;         // next 8-row group
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)BM * KTOT;
+  uint32_t* sEpi = reinterpret_cast<uint32_t*>(sB + (size_t)p.stages * kStageBytes);  // [8 warps][32][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiStageWords);
+  uint64_t* full = bars;                   // [stages] (leader): 2 CTAs x 4 producer warps
+  uint64_t* empty = bars + p.stages;       // [stages] (each CTA): MMA commit
+  uint64_t* tfull = bars + 2 * p.stages;   // [2] (each CTA): MMA commit
+  uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cr = cluster_ctarank();
+  const bool leader = cr == 0;
+  const int64_t pb = (int64_t)NB * 16, cb = 2 * pb;
+  const int S = p.stages;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), 2 * kProdWarps);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull[a]), 1);
+      mbar_init(smem_u32(&tempty[a]), 2 * 4 * kEpiSets);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc2(smem_u32(s_tmem), kTmemCols);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+
+  int stage = 0;            // producers: next stage to fill
+  uint32_t sphase = 0;
+  int mstage = 0;           // MMA issuer: next stage to consume
+  uint32_t mphase = 0;
+  int acc = 0;              // accumulator buffer (issuer and epilogue each track it)
+  uint32_t aphase = 0;
+
+  for (int64_t item = pair; item < p.n_items; item += npairs) {
+    const Item it = decode_item(p, item);
+    const int64_t q0 = (int64_t)it.t * (2 * BM) + (int64_t)cr * BM;  // this CTA's queries
+    const int64_t row0 = it.row0;
+    const int64_t rows = it.rows;
+    const int ntiles = (int)((rows + BN - 1) / BN);
+
+    // ---- A: this CTA's 128 query codes, expanded (all threads) ----
+    cluster_sync();  // previous item retired in both CTAs (A is read by the pair's MMAs)
+    for (int u = threadIdx.x; u < BM * NB; u += kThreads) {
+      const int r = u / NB, kb = u % NB;
+      uint4 qp = make_uint4(0, 0, 0, 0), qn = qp;
+      if (q0 + r < p.nq) {
+        const uint8_t* src = p.q + (q0 + r) * cb + kb * 16;
+        qp = *reinterpret_cast<const uint4*>(src);
+        qn = *reinterpret_cast<const uint4*>(src + pb);
+      }
+      expand_block_store(qp, qn, sA + (size_t)(kb * 8) * A_LBO + (r >> 3) * SBO + (r & 7) * 16, A_LBO);
+    }
+    fence_proxy_async();
+    cluster_sync();  // both CTAs' A tiles are in place before the leader issues
+
+    if (warp < kProdWarps) {
+      // ================= producers: rows [cr*128, cr*128+128) of each tile =================
+      const int r = threadIdx.x;
+      const uint32_t full_dst = mapa(smem_u32(&full[0]), 0);  // leader's full[0]
+      uint4 dp[NB], dn[NB];
+      auto load_block = [&](int tile, int kb, uint4& a, uint4& b) {
+        const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + r;
+        if (tile < ntiles && lr < rows && !(p.dbg & 4)) {
+          const uint8_t* src = p.db + (row0 + lr) * p.row_stride * cb;
+          a = __ldg(reinterpret_cast<const uint4*>(src) + kb);
+          b = __ldg(reinterpret_cast<const uint4*>(src + pb) + kb);
+        } else {
+          a = make_uint4(0, 0, 0, 0);
+          b = a;
+        }
+      };
+#pragma unroll
+      for (int kb = 0; kb < NB; ++kb) load_block(0, kb, dp[kb], dn[kb]);
+      for (int tile = 0; tile < ntiles; ++tile) {
+#pragma unroll
+        for (int kb = 0; kb < NB; ++kb) {
+          mbar_wait(smem_u32(&empty[stage]), sphase ^ 1u);
+          if (!(p.dbg & 1))
+            expand_block_store(dp[kb], dn[kb],
+                               sB + (size_t)stage * kStageBytes + (r >> 3) * SBO + (r & 7) * 16, B_LBO);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(full_dst + (uint32_t)stage * 8u);
+          if (++stage == S) { stage = 0; sphase ^= 1u; }
+          load_block(tile + 1, kb, dp[kb], dn[kb]);
+        }
+      }
+    } else if (warp == kMmaWarp) {
+      // ================= MMA issuer (leader CTA, one lane) =================
+      if (leader) {
+        constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+        const uint32_t a_addr = smem_u32(sA);
+        const uint32_t b_addr = smem_u32(sB);
+        for (int tile = 0; tile < ntiles; ++tile) {
+          if (lane == 0) {
+            mbar_wait_cluster(smem_u32(&tempty[acc]), aphase ^ 1u);  // accumulator drained (both CTAs)
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
+#pragma unroll 1
+            for (int kb = 0; kb < NB; ++kb) {
+              mbar_wait_cluster(smem_u32(&full[mstage]), mphase);      // both halves of B written
+              tc_fence_after();
+#pragma unroll
+              for (int ks = 0; ks < KB / 32; ++ks) {
+                const uint64_t ad = smem_desc(a_addr + (uint32_t)(kb * 8 + ks * 2) * A_LBO, A_LBO, SBO);
+                const uint64_t bd = smem_desc(b_addr + (uint32_t)mstage * kStageBytes + (uint32_t)(ks * 2) * B_LBO,
+                                              B_LBO, SBO);
+                mma2_i8(d_tmem, ad, bd, idesc, (kb | ks) != 0 ? 1u : 0u);
+              }
+              mma2_commit_mc(smem_u32(&empty[mstage]), 0x3);
+              if (++mstage == S) { mstage = 0; mphase ^= 1u; }
+            }
+            mma2_commit_mc(smem_u32(&tfull[acc]), 0x3);
+          }
+          __syncwarp();
+          if (++acc == 2) { acc = 0; aphase ^= 1u; }
+        }
+      }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 * kEpiSets) {
+      // ================= epilogue: per-query top-k streams =================
+      // set h handles accumulator columns [h*BN/2, (h+1)*BN/2) of every tile, so
+      // each query has kEpiSets streams, each seeing its rows in increasing order
+      const int ew = warp - kEpiWarp0;
+      const int quarter = ew & 3;             // == warp % 4: TMEM lane quarter
+      const int h = ew >> 2;                  // column half
+      const int sidx = h * BM + quarter * 32; // first stream of this warp
+      uint32_t* const wbufs = p.bufs + ((size_t)blockIdx.x * kEpiSets * BM + sidx) * p.cap;
+      uint32_t* const my_buf = wbufs + (size_t)lane * p.cap;
+      uint4* const srow = reinterpret_cast<uint4*>(sEpi + ((size_t)ew * 32 + lane) * 32);
+      const uint32_t tempty_dst = mapa(smem_u32(&tempty[0]), 0);  // leader's tempty[0]
+      const int64_t qme = q0 + quarter * 32 + lane;
+      int cnt = 0;
+      int thrd = INT32_MIN;  // a score passes iff Delta > thrd
+      if (p.thr0 && qme < p.nq) {
+        const int32_t dk = p.thr0[qme * p.thr0_stride];
+        if (dk != INT32_MIN) thrd = dk - 1;
+      }
+      constexpr int CW = BN / kEpiSets;       // columns per set per tile
+      for (int tile = 0; tile < ntiles; ++tile) {
+        mbar_wait(smem_u32(&tfull[acc]), aphase);
+        tc_fence_after();
+        const uint32_t tbase =
+            tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kAccStride) + (uint32_t)(h * CW);
+        const int64_t lr0 = (int64_t)tile * BN + h * CW;  // local row of this set's column 0
+        const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
+        // One 32-column group at a time.  Fast path: 4-score
+        // chunk maxima and one vote.  Slow path (compact code; the fully
+        // unrolled variant thrashed the instruction cache): stage the row in
+        // SMEM, then walk, warp-uniformly, only the chunks where some lane has
+        // a candidate.
+        auto process = [&](uint32_t (&v)[32], int c0) {
+          if (ncols - c0 < 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j >= ncols) v[j] = 0x80000000u;
+          }
+          int cm[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
+          const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
+                                      max(cm[6], cm[7]));
+          if (__any_sync(kFull, mx > thrd)) {
+            unsigned cmask = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              srow[i ^ (lane & 7)] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              cmask |= (cm[i] > thrd ? 1u : 0u) << i;
+            }
+            unsigned wmask = __reduce_or_sync(kFull, cmask);
+            while (wmask) {
+              const int i = __ffs(wmask) - 1;
+              wmask &= wmask - 1;
+              if ((cmask >> i) & 1u) {
+                const uint4 q4 = srow[i ^ (lane & 7)];
+                const uint32_t rb0 = (uint32_t)(lr0 + c0 + 4 * i);
+                if ((int)q4.x > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.x, rb0);
+                if ((int)q4.y > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.y, rb0 + 1);
+                if ((int)q4.z > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.z, rb0 + 2);
+                if ((int)q4.w > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.w, rb0 + 3);
+              }
+            }
+            __syncwarp();
+          }
+        };
+#pragma unroll 1
+        for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + (uint32_t)c0, v);
+          process(v, c0);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
+        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+        unsigned need = __ballot_sync(kFull, cnt > p.k + CW);
+        while (need) {
+          const int L = __ffs(need) - 1;
+          need &= need - 1;
+          const int cL = __shfl_sync(kFull, cnt, L);
+          const uint32_t D = ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
+          if (lane == L) {
+            cnt = p.k;
+            thrd = max(thrd, (int)D - p.kf.off);
+          }
+        }
+      }
+      // finalize: cut to k, publish global keys as list (chunk, set)
+      __syncwarp();
+      unsigned need = __ballot_sync(kFull, cnt > p.k);
+      while (need) {
+        const int L = __ffs(need) - 1;
+        need &= need - 1;
+        const int cL = __shfl_sync(kFull, cnt, L);
+        ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
+        if (lane == L) cnt = p.k;
+      }
+      __syncwarp();
+      for (int L = 0; L < 32; ++L) {
+        const int64_t qi = q0 + quarter * 32 + L;
+        const int cL = __shfl_sync(kFull, cnt, L);
+        if (qi >= p.nq) continue;
+        const uint32_t* bL = wbufs + (size_t)L * p.cap;
+        uint64_t* out = p.part + ((size_t)(it.c * kEpiSets + h) * p.nq + qi) * p.k;
+        for (int i = lane; i < p.k; i += 32)
+          out[i] = (i < cL) ? global_key_from_local(p.kf, bL[i], (uint64_t)row0) : 0ull;
+        if (it.c == it.s_t - 1)
+          for (int c2 = it.s_t; c2 < p.s_max; ++c2) {
+            uint64_t* z = p.part + ((size_t)(c2 * kEpiSets + h) * p.nq + qi) * p.k;
+            for (int i = lane; i < p.k; i += 32) z[i] = 0ull;
+          }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, kTmemCols);
+  }
+}
+
+}  // namespace tc2
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int tc2_stages(int NB) {
+  const int a_bytes = tc2::BM * NB * tc2::KB;
+  const int budget = 227 * 1024 - a_bytes - tc2::kEpiStageWords * 4 - 2048;
+  int s = budget / tc2::kStageBytes;
+  if (s > 8) s = 8;
+  return s;
+}
+
+// Pairs: the query set is cut into 256-query pair tiles; each of the SMs/2
+// pairs gets one (pair tile, DB chunk) item when the tiles do not cover them.
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  TcPlan pl{};
+  const int NB = blocks128(d);
+  pl.ok = false;
+  if (NB > 8 || nq < 1 || n < 1) return pl;
+  pl.stages = tc2_stages(NB);
+  if (pl.stages < 2) return pl;
+  pl.ok = true;
+  const int npairs = sms / 2;
+  pl.n_qtiles = (int32_t)((nq + 2 * tc2::BM - 1) / (2 * tc2::BM));
+  pl.cap = k + 2 * (tc2::BN / tc2::kEpiSets);
+  const KeyFmt kf = make_keyfmt(d);
+  const int64_t lmax = ((int64_t)kf.rmask + 1) / tc2::BN * tc2::BN;
+  const int64_t s_min = (n + lmax - 1) / lmax;
+  int64_t s_cap = (n + 4 * tc2::BN - 1) / (4 * tc2::BN);
+  if (s_cap < s_min) s_cap = s_min;
+  const int64_t QT = pl.n_qtiles;
+  if (QT * s_min >= npairs) {
+    pl.s_lo = (int32_t)s_min;
+    pl.r_hi = 0;
+  } else {
+    int64_t lo = npairs / QT, hi = npairs % QT;
+    if (lo >= s_cap) { lo = s_cap; hi = 0; }
+    pl.s_lo = (int32_t)lo;
+    pl.r_hi = (int32_t)hi;
+  }
+  const int32_t s_max = pl.s_lo + (pl.r_hi > 0 ? 1 : 0);
+  pl.n_chunks = (int64_t)s_max * tc2::kEpiSets;  // lists per query for the merge
+  pl.n_items = QT * pl.s_lo + pl.r_hi;
+  const int64_t pairs = pl.n_items < npairs ? pl.n_items : npairs;
+  pl.grid = (int32_t)(2 * pairs);
+  pl.smem = 1024 + tc2::BM * NB * tc2::KB + pl.stages * tc2::kStageBytes + tc2::kEpiStageWords * 4 +
+            (2 * pl.stages + 4) * 8 + 16;
+  pl.buf_bytes = (size_t)pl.grid * tc2::kEpiSets * tc2::BM * pl.cap * 4;
+  pl.part_bytes = (size_t)pl.n_chunks * nq * k * 8;
+  return pl;
+}
+
+template <int NB>
+static cudaError_t launch_tc2_nb(const tc2::Params& p, const TcPlan& pl, cudaStream_t st) {
+  auto kern = tc2::scan_tc2_kernel<NB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
+  if (e != cudaSuccess) return e;
+  kern<<<pl.grid, tc2::kThreads, pl.smem, st>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
+                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
+                            cudaStream_t st) {
+  const int NB = blocks128(d);
+  static const int dbg = [] {
+    const char* e = getenv("UQ_TC_ABLATE");
+    return e ? atoi(e) : 0;
+  }();
+  tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
+                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, bufs, part, thr0, thr0_stride,
+                row_stride, dbg};
+  switch (NB) {
+    case 1: return launch_tc2_nb<1>(p, pl, st);
+    case 2: return launch_tc2_nb<2>(p, pl, st);
+    case 3: return launch_tc2_nb<3>(p, pl, st);
+    case 4: return launch_tc2_nb<4>(p, pl, st);
+    case 5: return launch_tc2_nb<5>(p, pl, st);
+    case 6: return launch_tc2_nb<6>(p, pl, st);
+    case 7: return launch_tc2_nb<7>(p, pl, st);
+    case 8: return launch_tc2_nb<8>(p, pl, st);
+    default: break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace uq

@@ -153,6 +153,14 @@ def test_search_parity_ties(uq, orc, algo, mode):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("mode,n,k", [("dup", 131072, 100), ("ties", 100000, 10), ("normal", 70001, 1)])
+def test_search_parity_seeded(uq, orc, algo, mode, n, k):
+    """n >= 2^16 turns on threshold seeding (a strided-sample pre-scan); exactness must
+    hold with massive ties at the seeded threshold."""
+    _search_case(uq, orc, algo, 128, 64, n, 130, k, seed=11, mode=mode)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 def test_search_c1_full(uq, orc, algo):
     """BASELINE config 1 at full size (N=10,000, Q=100, d=384, x=192, k=10)."""
     w = datagen.CONFIGS["c1"]
