@@ -154,6 +154,14 @@ uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d,
  */
 uq_status uq_timing_enable(int32_t on);
 uq_status uq_timing_collect(double* scan_ms, int64_t* launches);
+/*
+ * uq_timing_collect_ex -- as uq_timing_collect, split by launch kind: index 0 =
+ * main scans (every database row), index 1 = threshold-seeding scans over a
+ * strided sample.  scan_ms[2], launches[2] and delta_evals[2] (host arrays)
+ * receive the summed kernel time, the launch count and the summed Delta
+ * evaluations (nq x rows) of each kind.  Resets the record.
+ */
+uq_status uq_timing_collect_ex(double* scan_ms, int64_t* launches, double* delta_evals);
 
 /*
  * uq_last_launches -- number of kernels the most recent uq_* call on this

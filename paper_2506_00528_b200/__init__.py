@@ -17,7 +17,7 @@ import torch
 __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
     "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05",
-    "last_launches", "version", "timing_enable", "timing_collect",
+    "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -54,7 +54,9 @@ def _load():
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
     L.uq_timing_enable.argtypes = [i32]
     L.uq_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
-    for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
+    L.uq_timing_collect_ex.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
+                                       ctypes.POINTER(ctypes.c_double)]
+    for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_timing_collect_ex", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
               "uq_check_codes"):
         getattr(L, f).restype = i32
     return L
@@ -86,6 +88,17 @@ def timing_collect() -> Tuple[float, int]:
     ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
     _check("uq_timing_collect", _L.uq_timing_collect(ctypes.byref(ms), ctypes.byref(n)))
     return float(ms.value), int(n.value)
+
+
+def timing_collect_ex() -> dict:
+    """Scan-kernel timing split by kind: {"main": (ms, launches, delta_evals),
+    "seed": (...)} since the last collect."""
+    ms = (ctypes.c_double * 2)()
+    n = (ctypes.c_int64 * 2)()
+    ev = (ctypes.c_double * 2)()
+    _check("uq_timing_collect_ex", _L.uq_timing_collect_ex(ms, n, ev))
+    return {"main": (float(ms[0]), int(n[0]), float(ev[0])),
+            "seed": (float(ms[1]), int(n[1]), float(ev[1]))}
 
 
 def code_bytes(d: int) -> int:

@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libuq.so (declared and documented in include/uq.h):
 // synchronous argument validation, launch planning, workspace carving.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -17,6 +18,7 @@ void note_launch(int n) { g_launches += n; }
 struct ScanTimer {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<std::pair<int, double>> tag;  // (0 main scan / 1 seed scan, Delta evaluations)
   size_t used = 0;
   ~ScanTimer() {
     for (auto& p : ev) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -24,7 +26,7 @@ struct ScanTimer {
 };
 static thread_local ScanTimer g_timer;
 
-static void timer_begin(cudaStream_t st, cudaEvent_t* stop) {
+static void timer_begin(cudaStream_t st, cudaEvent_t* stop, int kind, double evals) {
   *stop = nullptr;
   if (!g_timer.on) return;
   if (g_timer.used == g_timer.ev.size()) {
@@ -32,7 +34,9 @@ static void timer_begin(cudaStream_t st, cudaEvent_t* stop) {
     if (cudaEventCreate(&a) != cudaSuccess) return;
     if (cudaEventCreate(&b) != cudaSuccess) { cudaEventDestroy(a); return; }
     g_timer.ev.emplace_back(a, b);
+    g_timer.tag.emplace_back(0, 0.0);
   }
+  g_timer.tag[g_timer.used] = {kind, evals};
   auto& p = g_timer.ev[g_timer.used++];
   cudaEventRecord(p.first, st);
   *stop = p.second;
@@ -101,8 +105,13 @@ struct SeedPlan {
 };
 static SeedPlan plan_seed(int64_t n, int32_t k) {
   SeedPlan sp{false, 0, 1};
+  static const int seed_div = [] {
+    const char* e = getenv("UQ_SEED_DIV");  // experiment knob: 0 disables seeding
+    return e ? atoi(e) : 32;
+  }();
+  if (seed_div <= 0) return sp;
   if (n < (int64_t)1 << 16) return sp;
-  int64_t rows = n / 32;
+  int64_t rows = n / seed_div;
   if (rows < 16 * (int64_t)k) return sp;
   sp.on = true;
   sp.stride = n / rows;
@@ -153,11 +162,11 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
                                   int32_t d, int32_t k, int64_t id_base, int64_t row_stride,
                                   const int32_t* thr0, int32_t thr0_stride, uint32_t* bufs,
                                   uint64_t* part, int32_t* out_s, int64_t* out_id, int sms,
-                                  cudaStream_t st) {
+                                  int timer_kind, cudaStream_t st) {
   cudaEvent_t ev;
   int64_t lists = 0;
   cudaError_t e;
-  timer_begin(st, &ev);
+  timer_begin(st, &ev, timer_kind, (double)nq * (double)n);
   if (a == UQ_ALGO_TCGEN05) {
     const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
     e = use_pairs(nq) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st)
@@ -201,19 +210,31 @@ uq_status uq_timing_enable(int32_t on) {
   return UQ_OK;
 }
 
-uq_status uq_timing_collect(double* scan_ms, int64_t* launches) {
-  if (!scan_ms || !launches) return UQ_ERR_INVALID_ARG;
-  double tot = 0.0;
+uq_status uq_timing_collect_ex(double* scan_ms, int64_t* launches, double* delta_evals) {
+  if (!scan_ms || !launches || !delta_evals) return UQ_ERR_INVALID_ARG;
+  for (int j = 0; j < 2; ++j) { scan_ms[j] = 0.0; launches[j] = 0; delta_evals[j] = 0.0; }
   for (size_t i = 0; i < g_timer.used; ++i) {
     auto& p = g_timer.ev[i];
     if (cudaEventSynchronize(p.second) != cudaSuccess) return UQ_ERR_CUDA;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.first, p.second) != cudaSuccess) return UQ_ERR_CUDA;
-    tot += ms;
+    const int j = g_timer.tag[i].first;
+    scan_ms[j] += ms;
+    launches[j] += 1;
+    delta_evals[j] += g_timer.tag[i].second;
   }
-  *scan_ms = tot;
-  *launches = (int64_t)g_timer.used;
   g_timer.used = 0;
+  return UQ_OK;
+}
+
+uq_status uq_timing_collect(double* scan_ms, int64_t* launches) {
+  if (!scan_ms || !launches) return UQ_ERR_INVALID_ARG;
+  double ms[2], ev[2];
+  int64_t n[2];
+  const uq_status s = uq_timing_collect_ex(ms, n, ev);
+  if (s != UQ_OK) return s;
+  *scan_ms = ms[0] + ms[1];
+  *launches = n[0] + n[1];
   return UQ_OK;
 }
 
@@ -295,13 +316,13 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
     int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
     cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, sp.rows, d, k, 0, sp.stride, nullptr, 0,
-                                   bufs, part, seed_s, seed_i, sms, st);
+                                   bufs, part, seed_s, seed_i, sms, 1, st);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = seed_s + (k - 1);  // k-th best sample Delta, row stride k
   }
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
   cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, k, bufs, part,
-                                 out_scores, out_ids, sms, st);
+                                 out_scores, out_ids, sms, 0, st);
   return from_cuda(e);
 }
 

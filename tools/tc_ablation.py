@@ -20,6 +20,6 @@ else:
     n, nq, k = (sys.argv[1:4] if len(sys.argv) > 3 else ("1000000", "1000", "100"))
     n, nq, k = str(n), str(nq), str(k)
     for mode in sys.argv[4:] if len(sys.argv) > 4 else ("0", "2", "3", "7"):
-        env = dict(os.environ, UQ_TC_ABLATE=mode)
+        env = dict(os.environ, UQ_TC_ABLATE=mode, UQ_SEED_DIV="0")
         r = subprocess.run([sys.executable, __file__, "child", n, nq, k], env=env, capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-500:], flush=True)
