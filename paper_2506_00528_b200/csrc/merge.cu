@@ -5,16 +5,19 @@
 // Exactness: the global top-k under a total order is a subset of the union of
 // the per-list top-k's, so selecting the k largest keys of the union is exact.
 //
-// One CTA per query: (1) T = k-th largest key by bisection over the 64 key
-// bits with block-wide counts; (2) gather the <= k keys >= T into shared
-// memory; (3) bitonic sort descending; (4) write (score, id) best first,
-// padding with (INT32_MIN, -1).
+// One CTA per query: (1) T = k-th largest valid key by an MSB-first radix
+// select (8-bit digits, shared-memory histogram per digit, starting at the
+// highest bit in which the candidates differ, early exit once a whole digit
+// bucket is taken); (2) gather the <= k keys >= T into shared memory; (3) rank
+// each selected key by counting the larger ones (keys are unique) and write
+// (score, id) at its rank, padding with (INT32_MIN, -1).
 #include "common.cuh"
 #include "internal.h"
 
 namespace uq {
 
 constexpr int kMergeThreads = 256;
+constexpr int kMergeWarps = kMergeThreads / 32;
 
 struct MergeParams {
   // source (a): keys [lists][nq][k]; source (b): scores/ids [lists][nq][k]
@@ -39,83 +42,121 @@ __device__ __forceinline__ uint64_t cand_key(const MergeParams& p, int64_t q, in
   return p.keys[off];
 }
 
-__device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* s_acc) {
-  v = __reduce_add_sync(kFull, v);
-  if ((threadIdx.x & 31) == 0) atomicAdd(s_acc, v);
-  __syncthreads();
-  const unsigned tot = *s_acc;
-  __syncthreads();
-  if (threadIdx.x == 0) *s_acc = 0;
-  __syncthreads();
-  return tot;
-}
+// (key >> r) with r in [0, 64]
+__device__ __forceinline__ uint64_t shr64(uint64_t v, int r) { return r >= 64 ? 0ull : (v >> r); }
 
 template <bool FROM_SI>
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   extern __shared__ uint64_t smem_u64[];
-  __shared__ unsigned s_acc;
+  __shared__ unsigned s_hist[256];
+  __shared__ unsigned long long s_and[kMergeWarps], s_or[kMergeWarps];
+  __shared__ unsigned s_cnt[kMergeWarps];
   __shared__ int s_nsel;
+  __shared__ int s_b, s_above, s_inb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = blockIdx.x;
   const int64_t C = p.lists * p.kin;
   const int P = 1 << bitlen((unsigned)(p.k - 1 > 0 ? p.k - 1 : 1));  // pow2 >= k (>= 2)
   uint64_t* s_sel = smem_u64;          // [P]
   uint64_t* s_cand = smem_u64 + P;     // [stage_cap] (if staged)
   const bool staged = C <= p.stage_cap;
-  if (threadIdx.x == 0) { s_acc = 0; s_nsel = 0; }
-  if (staged)
-    for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) s_cand[i] = cand_key<FROM_SI>(p, q, i);
+  // stage + common bits of the valid (non-zero) keys
+  uint64_t a_and = ~0ull, a_or = 0ull;
+  unsigned nv = 0;
+  for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) {
+    const uint64_t key = cand_key<FROM_SI>(p, q, i);
+    if (staged) s_cand[i] = key;
+    if (key != 0ull) { a_and &= key; a_or |= key; ++nv; }
+  }
+  a_and = __reduce_and_sync(kFull, (unsigned)a_and) | ((uint64_t)__reduce_and_sync(kFull, (unsigned)(a_and >> 32)) << 32);
+  a_or = __reduce_or_sync(kFull, (unsigned)a_or) | ((uint64_t)__reduce_or_sync(kFull, (unsigned)(a_or >> 32)) << 32);
+  nv = __reduce_add_sync(kFull, nv);
+  if (lane == 0) { s_and[warp] = a_and; s_or[warp] = a_or; s_cnt[warp] = nv; }
+  if (threadIdx.x == 0) s_nsel = 0;
   __syncthreads();
+  uint64_t all_and = ~0ull, all_or = 0ull;
+  unsigned nvalid = 0;
+#pragma unroll
+  for (int w = 0; w < kMergeWarps; ++w) { all_and &= s_and[w]; all_or |= s_or[w]; nvalid += s_cnt[w]; }
   auto get = [&](int64_t i) -> uint64_t { return staged ? s_cand[i] : cand_key<FROM_SI>(p, q, i); };
 
-  // (1) T = k-th largest key (max T with #{key >= T} >= k)
-  uint64_t T = 0;
-  for (int b = 63; b >= 0; --b) {
-    const uint64_t cand = T | (1ull << b);
-    unsigned c = 0;
-    for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) c += get(i) >= cand ? 1u : 0u;
-    const unsigned tot = block_sum(c, &s_acc);
-    if (tot >= (unsigned)p.k) {
-      T = cand;
-      if (tot == (unsigned)p.k) break;
+  // (1) T = k-th largest valid key
+  uint64_t T = 1ull;  // fewer than k valid candidates: take every valid one
+  if (nvalid > (unsigned)p.k) {
+    const uint64_t diff = all_and ^ all_or;      // != 0: keys are unique
+    int r = 64 - __clzll((long long)diff);       // bits [r, 64) are common to every valid key
+    uint64_t prefix = (r >= 64) ? 0ull : (all_and >> r) << r;
+    int krem = p.k;
+    while (r > 0) {
+      const int w = r < 8 ? r : 8;
+      const int sh = r - w;
+      const unsigned dmask = (1u << w) - 1u;
+      s_hist[threadIdx.x] = 0u;
+      __syncthreads();
+      const uint64_t hi = shr64(prefix, r);
+      for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) {
+        const uint64_t key = get(i);
+        if (key != 0ull && shr64(key, r) == hi) atomicAdd(&s_hist[(unsigned)(key >> sh) & dmask], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // lane l owns bins [248 - 8l, 255 - 8l] (descending digit order)
+        unsigned c[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { c[j] = s_hist[255 - 8 * lane - j]; sum += c[j]; }
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += t;
+        }
+        unsigned above = incl - sum;  // keys in bins of higher-numbered lanes' ranges (larger digits)
+        const bool mine = above < (unsigned)krem && incl >= (unsigned)krem;
+        if (mine) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (above < (unsigned)krem && above + c[j] >= (unsigned)krem) {
+              s_b = 255 - 8 * lane - j;
+              s_above = (int)above;
+              s_inb = (int)c[j];
+            }
+            above += c[j];
+          }
+        }
+      }
+      __syncthreads();
+      const int b = s_b;
+      krem -= s_above;
+      prefix |= (uint64_t)b << sh;
+      r = sh;
+      if (krem == s_inb) break;  // the whole bucket is taken: T = its smallest possible key
+      __syncthreads();           // s_hist / s_b reused by the next digit
     }
+    T = prefix;
   }
-  if (T == 0) T = 1;  // fewer than k valid candidates: take every valid one
-  // (2) gather
-  for (int i = threadIdx.x; i < P; i += kMergeThreads) s_sel[i] = 0ull;
-  __syncthreads();
+  // (2) gather the keys >= T (exactly min(k, nvalid): keys are unique)
   for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) {
     const uint64_t key = get(i);
-    if (key >= T) {
+    if (key != 0ull && key >= T) {
       const int pos = atomicAdd(&s_nsel, 1);
       if (pos < P) s_sel[pos] = key;
     }
   }
   __syncthreads();
-  // (3) bitonic sort, descending
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P; i += kMergeThreads) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool desc = ((i & size) == 0);
-          const uint64_t a = s_sel[i], b = s_sel[j];
-          if (desc ? (a < b) : (a > b)) { s_sel[i] = b; s_sel[j] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // (4) write
-  for (int i = threadIdx.x; i < p.k; i += kMergeThreads) {
+  const int nsel = s_nsel < p.k ? s_nsel : p.k;
+  // (3) rank by counting (distinct keys) and write best first
+  for (int i = threadIdx.x; i < nsel; i += kMergeThreads) {
     const uint64_t key = s_sel[i];
+    int rank = 0;
+    for (int j = 0; j < nsel; ++j) rank += (s_sel[j] > key) ? 1 : 0;
+    const size_t o = (size_t)q * p.k + rank;
+    p.out_s[o] = key_score(key);
+    p.out_id[o] = (FROM_SI ? 0 : p.id_base) + key_row(key);
+  }
+  for (int i = nsel + threadIdx.x; i < p.k; i += kMergeThreads) {
     const size_t o = (size_t)q * p.k + i;
-    if (key == 0) {
-      p.out_s[o] = INT32_MIN;
-      p.out_id[o] = -1;
-    } else {
-      p.out_s[o] = key_score(key);
-      p.out_id[o] = (FROM_SI ? 0 : p.id_base) + key_row(key);
-    }
+    p.out_s[o] = INT32_MIN;
+    p.out_id[o] = -1;
   }
 }
 
