@@ -103,12 +103,16 @@ struct SeedPlan {
   bool on;
   int64_t rows, stride;
 };
-static SeedPlan plan_seed(int64_t n, int32_t k) {
+// Histogram seeding (CTA-pair tensor engine): a cheap epilogue, so a denser
+// sample (1/8) buys a tighter bound.  Top-k seeding (other engines): 1/32.
+static bool hist_seed(uq_algo a, int64_t nq) { return a == UQ_ALGO_TCGEN05 && use_pairs(nq); }
+static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
   SeedPlan sp{false, 0, 1};
-  static const int seed_div = [] {
+  static const int div_env = [] {
     const char* e = getenv("UQ_SEED_DIV");  // experiment knob: 0 disables seeding
-    return e ? atoi(e) : 32;
+    return e ? atoi(e) : -1;
   }();
+  const int seed_div = div_env >= 0 ? div_env : (hist ? 8 : 32);
   if (seed_div <= 0) return sp;
   if (n < (int64_t)1 << 16) return sp;
   int64_t rows = n / seed_div;
@@ -120,7 +124,7 @@ static SeedPlan plan_seed(int64_t n, int32_t k) {
 }
 
 struct SearchLayout {
-  size_t bufs_off, part_off, seed_s_off, seed_i_off, total;
+  size_t bufs_off, part_off, seed_s_off, seed_i_off, hist_off, total;
 };
 
 static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms,
@@ -136,20 +140,22 @@ static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t 
 }
 
 static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  SearchLayout L{0, 0, 0, 0, 0};
+  SearchLayout L{0, 0, 0, 0, 0, 0};
   if (nq == 0 || n == 0) return L;
   size_t bufs = 0, part = engine_bytes(a, nq, n, d, k, sms, &bufs);
-  const SeedPlan sp = plan_seed(n, k);
-  if (sp.on) {
+  const bool hist = hist_seed(a, nq);
+  const SeedPlan sp = plan_seed(n, k, hist);
+  if (sp.on && !hist) {
     size_t b2 = 0, p2 = engine_bytes(a, nq, sp.rows, d, k, sms, &b2);
     if (b2 > bufs) bufs = b2;
     if (p2 > part) part = p2;
   }
   L.bufs_off = 0;
   L.part_off = bufs;
-  L.seed_s_off = L.part_off + part;
-  L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * k * 4, 256) : 0);
-  L.total = L.seed_i_off + (sp.on ? align_up((size_t)nq * k * 8, 256) : 0);
+  L.seed_s_off = L.part_off + part;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
+  L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * (hist ? 1 : k) * 4, 256) : 0);
+  L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
+  L.total = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 128 * 4, 256) : 0);
   return L;
 }
 
@@ -208,6 +214,12 @@ int32_t uq_last_launches(void) { return g_launches; }
 uq_status uq_timing_enable(int32_t on) {
   g_timer.on = on != 0;
   return UQ_OK;
+}
+
+// Debug (not in uq.h): CTA-pair scan cycle accounting under UQ_TC_ABLATE & 8.
+uq_status uq_debug_tc2_prof(unsigned long long* out16) {
+  if (!out16) return UQ_ERR_INVALID_ARG;
+  return from_cuda(tc2_prof_read(out16));
 }
 
 uq_status uq_timing_collect_ex(double* scan_ms, int64_t* launches, double* delta_evals) {
@@ -310,9 +322,23 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   const SearchLayout L = layout_for(a, nq, n, d, k, sms);
   uint32_t* bufs = reinterpret_cast<uint32_t*>(ws + L.bufs_off);
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part_off);
-  const SeedPlan sp = plan_seed(n, k);
+  const bool hist = hist_seed(a, nq);
+  const SeedPlan sp = plan_seed(n, k, hist);
   const int32_t* thr0 = nullptr;
-  if (sp.on) {
+  int32_t thr0_stride = k;
+  if (sp.on && hist) {
+    // Delta histogram of a strided sample -> per-query lower bound on D_k
+    int32_t* thr = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
+    uint32_t* ghist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
+    if (cudaMemsetAsync(ghist, 0, (size_t)nq * 128 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
+    cudaEvent_t ev;
+    timer_begin(st, &ev, 1, (double)nq * (double)sp.rows);
+    cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, sp.stride, ghist, thr, sms, st);
+    timer_end(st, ev);
+    if (e != cudaSuccess) return UQ_ERR_CUDA;
+    thr0 = thr;
+    thr0_stride = 1;
+  } else if (sp.on) {
     int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
     int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
     cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, sp.rows, d, k, 0, sp.stride, nullptr, 0,
@@ -321,7 +347,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     thr0 = seed_s + (k - 1);  // k-th best sample Delta, row stride k
   }
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
-  cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, k, bufs, part,
+  cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, thr0_stride, bufs, part,
                                  out_scores, out_ids, sms, 0, st);
   return from_cuda(e);
 }

@@ -359,7 +359,7 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
 
 // Phi^-1(p) for p in (0, 1) (Acklam's rational approximation; only steers the
 // probes of the search, never decides a bit)
-static float inv_norm_cdf(double p) {
+float inv_norm_cdf(double p) {
   static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
                              1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
   static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,

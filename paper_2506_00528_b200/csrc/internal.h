@@ -11,6 +11,9 @@ namespace uq {
 
 void note_launch(int n = 1);
 
+// Phi^-1(p) (rational approximation; steering heuristics only, never a result)
+float inv_norm_cdf(double p);
+
 cudaError_t launch_encode(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld, int32_t x,
                           uint8_t* codes, int sms, cudaStream_t st);
 cudaError_t launch_scores(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
@@ -51,6 +54,11 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
 
 // Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128.
 TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+cudaError_t tc2_prof_read(unsigned long long* out16);
+TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms,
+                                 cudaStream_t st);
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,

@@ -3,22 +3,34 @@
 //
 // Same contraction as scan_tc.cu (Delta = T_q . T_db^T over {-1,0,1}, s32,
 // exact; P:209-216 / P:385-389) on a 2-CTA cluster: the pair computes a
-// 256-query x 192-row tile per K step.  CTA r of the pair
+// 256-query x 192-row tile.  CTA r of the pair
 //   * keeps its own 128 queries resident in SMEM (A, 128 x 128*NB int8),
 //   * expands only rows [96 r, 96 r + 96) of each 192-row DB tile (its half
 //     of B), so each SM expands half as many DB rows per unit of MMA work as
 //     the one-CTA kernel -- the expansion is the per-SM instruction bottleneck,
 //   * holds the 128 x 192 s32 accumulator of its own queries in TMEM (two
-//     buffers) and runs their top-k streams in its epilogue warps.
-// The leader CTA (rank 0) issues the MMAs; its `full` barriers count the
-// producer warps of both CTAs (the peer arrives through shared::cluster), the
-// MMA commits multicast to both CTAs' `empty` / `tfull` barriers, and both
-// CTAs' epilogue warps arrive on the leader's `tempty`.
+//     buffers) and runs their epilogue in its epilogue warps.
+// A pipeline stage carries 256 dims (two 128-dim blocks, 8 MMAs of K=32): the
+// per-stage barrier round trip (producers of both CTAs -> leader `full`, MMA
+// commit -> both CTAs' `empty`) costs about as much as four MMAs, so 8 MMAs per
+// stage keep the tensor pipe busy (tools/mma_bench.cu replica: 4 MMAs/stage
+// 3.2 POPS, 8 MMAs/stage 4.4 POPS at N = 192).
+//
+// Two epilogue modes:
+//   kTopK  per-query top-k streams (threshold filter in registers, append to
+//          a per-stream buffer, warp-cooperative cut back to k), lists of
+//          64-bit global keys per (chunk, column half) for the merge kernel;
+//   kHist  threshold seeding: per-query histogram of Delta >= F in bins of
+//          2^hshift (shared-memory atomics, flushed to a global [nq][128]
+//          histogram; F ~ 2 sigma of unrelated-code Delta filters ~98% first).  At least sum_{b' >= b} hist[b'] rows have Delta >=
+//          b << hshift, so thr_from_hist_kernel's per-query bound is exact.
 //
 // Warps: 0-2 producers (one thread per DB row of this CTA's 96-row half),
 // 3 MMA issuer (leader) + TMEM owner, 4-11 epilogue in two sets of four
 // (warp % 4 = TMEM lane quarter; set h reads accumulator columns
-// [96 h, 96 h + 96)).  N = 192 per pair tile.
+// [96 h, 96 h + 96)).  12 warps = 3 per SM sub-partition, whose 16K-register
+// file then allows 168 registers per thread (a 13th warp would cap it at 128).
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -33,16 +45,20 @@ using namespace ::uq::tc;
 constexpr int BM = 128;               // queries per CTA (pair M = 256)
 constexpr int BN = 192;               // DB rows per pair tile (UMMA N)
 constexpr int BH = BN / 2;            // DB rows expanded per CTA (96: three producer warps)
-constexpr int KB = 128;               // K bytes (dims) per stage
+constexpr int KB = 128;               // dims per expansion block (one uint4 of each plane)
+constexpr int kBlkPerStage = 2;       // 256 dims per pipeline stage
 constexpr int kProdWarps = 3;         // warps 0-2
 constexpr int kMmaWarp = 3;           // warp 3: MMA issuer (leader) + TMEM owner
 constexpr int kEpiSets = 2;           // epilogue warp sets, each owns half of a tile's columns
 constexpr int kEpiWarp0 = 4;          // warps 4..11 (warp % 4 = TMEM lane quarter)
 constexpr int kThreads = (4 + 4 * kEpiSets) * 32;  // 12 warps: 3 per SMSP -> 168 regs
 constexpr int kAccStride = 256;       // TMEM column offset of the second accumulator
-constexpr int kStageBytes = BH * KB;  // 16 KB per CTA per stage
+constexpr int kBlkBytes = BH * KB;    // 12 KB per CTA per 128-dim block
+constexpr int kStageBytes = kBlkPerStage * kBlkBytes;  // 24 KB
 constexpr uint32_t kTmemCols = 512;   // two s32 accumulators (columns 0 and 256)
-constexpr int kEpiStageWords = 4 * 2 * 32 * 32;  // epilogue staging: one 32-score row per thread
+constexpr int kHistBins = 128;
+constexpr int kHistBytes = (kHistBins / 2) * BM * 4;   // [64 words][128 queries], two u16 counts per word
+constexpr int kModeTopK = 0, kModeHist = 1;
 
 struct Params {
   const uint8_t* q;
@@ -62,8 +78,20 @@ struct Params {
   const int32_t* thr0;  // optional per-query seed D_k (rows with Delta < D_k cannot matter)
   int32_t thr0_stride;
   int64_t row_stride;
+  uint32_t* ghist;      // kHist: [nq][kHistBins]
+  int32_t hshift;       // kHist: bin = Delta >> hshift
+  float zfloor;         // kHist: only Delta >= zfloor * nnz(q) / sqrt(d) is counted
   int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads
 };
+
+// Cycle accounting (ablation/profiling only: dbg & 8), read by uq_tc2_prof:
+// 0 MMA item loop, 1 MMA wait tempty, 2 MMA wait full, 3 producer loop, 4
+// producer wait empty, 5 epilogue loop, 6 epilogue wait tfull, 7 epilogue
+// TMEM load + filter, 8 epilogue rebuilds, 9 epilogue publish, 10 items.
+__device__ unsigned long long g_prof[16];
+__device__ __forceinline__ long long clk() { return clock64(); }
+#define PROF_ON (MODE == kModeTopK && (p.dbg & 8))
+#define PROF_ADD(i, v) do { if (PROF_ON && lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(v)); } while (0)
 
 struct Item {
   int t, c, s_t;
@@ -92,22 +120,36 @@ __device__ __forceinline__ Item decode_item(const Params& p, int64_t i) {
   return it;
 }
 
-template <int NB>
+// kHist: add this thread's histogram column (query `qi`) to the global one and clear it
+__device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* g) {
+#pragma unroll 4
+  for (int w = 0; w < kHistBins / 2; ++w) {
+    uint32_t* cell = s_hist + w * BM + col;
+    const uint32_t v = atomicExch(cell, 0u);
+    if (g != nullptr) {
+      if (v & 0xffffu) atomicAdd(g + 2 * w, v & 0xffffu);
+      if (v >> 16) atomicAdd(g + 2 * w + 1, v >> 16);
+    }
+  }
+}
+
+template <int NB, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc2_kernel(Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   constexpr int KTOT = NB * KB;
+  constexpr int NST = (NB + kBlkPerStage - 1) / kBlkPerStage;  // stages per tile
   constexpr uint32_t A_LBO = BM * 16;   // next 16-B K chunk of A (128 rows)
   constexpr uint32_t B_LBO = BH * 16;   // next 16-B K chunk of this CTA's B half
   constexpr uint32_t SBO = 128;         // next 8-row group
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)BM * KTOT;
-  uint32_t* sEpi = reinterpret_cast<uint32_t*>(sB + (size_t)p.stages * kStageBytes);  // [8 warps][32][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiStageWords);
-  uint64_t* full = bars;                   // [stages] (leader): 2 CTAs x 4 producer warps
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(sB + (size_t)p.stages * kStageBytes);  // kHist only
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s_hist) + (MODE == kModeHist ? kHistBytes : 0));
+  uint64_t* full = bars;                   // [stages] (leader): 2 CTAs x producer warps
   uint64_t* empty = bars + p.stages;       // [stages] (each CTA): MMA commit
   uint64_t* tfull = bars + 2 * p.stages;   // [2] (each CTA): MMA commit
-  uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps
+  uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps per set
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -128,6 +170,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
     }
     fence_barrier_init();
   }
+  if (MODE == kModeHist)
+    for (int i = threadIdx.x; i < kHistBytes / 4; i += kThreads) s_hist[i] = 0u;
   if (warp == kMmaWarp) tmem_alloc2(smem_u32(s_tmem), kTmemCols);
   tc_fence_before();
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
@@ -164,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
     cluster_sync();  // both CTAs' A tiles are in place before the leader issues
 
     if (warp < kProdWarps) {
-      // ================= producers: rows [cr*128, cr*128+128) of each tile =================
+      // ================= producers: rows [cr*96, cr*96+96) of each tile =================
       const int r = threadIdx.x;
       const uint32_t full_dst = mapa(smem_u32(&full[0]), 0);  // leader's full[0]
       uint4 dp[NB], dn[NB];
@@ -181,41 +225,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       };
 #pragma unroll
       for (int kb = 0; kb < NB; ++kb) load_block(0, kb, dp[kb], dn[kb]);
+      long long t_loop = PROF_ON ? clk() : 0, t_wait = 0;
       for (int tile = 0; tile < ntiles; ++tile) {
 #pragma unroll
-        for (int kb = 0; kb < NB; ++kb) {
+        for (int ks = 0; ks < NST; ++ks) {
+          long long t0 = PROF_ON ? clk() : 0;
           mbar_wait(smem_u32(&empty[stage]), sphase ^ 1u);
-          if (!(p.dbg & 1))
-            expand_block_store(dp[kb], dn[kb],
-                               sB + (size_t)stage * kStageBytes + (r >> 3) * SBO + (r & 7) * 16, B_LBO);
+          if (PROF_ON) t_wait += clk() - t0;
+          uint8_t* sdst = sB + (size_t)stage * kStageBytes + (r >> 3) * SBO + (r & 7) * 16;
+#pragma unroll
+          for (int bb = 0; bb < kBlkPerStage; ++bb) {
+            const int kb = ks * kBlkPerStage + bb;
+            if (kb < NB) {
+              if (!(p.dbg & 1)) expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * 8) * B_LBO, B_LBO);
+              load_block(tile + 1, kb, dp[kb], dn[kb]);
+            }
+          }
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(full_dst + (uint32_t)stage * 8u);
           if (++stage == S) { stage = 0; sphase ^= 1u; }
-          load_block(tile + 1, kb, dp[kb], dn[kb]);
         }
       }
+      PROF_ADD(3, clk() - t_loop);
+      PROF_ADD(4, t_wait);
     } else if (warp == kMmaWarp) {
       // ================= MMA issuer (leader CTA, one lane) =================
       if (leader) {
         constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
         const uint32_t a_addr = smem_u32(sA);
         const uint32_t b_addr = smem_u32(sB);
+        long long t_loop = PROF_ON ? clk() : 0, t_we = 0, t_wf = 0;
         for (int tile = 0; tile < ntiles; ++tile) {
           if (lane == 0) {
+            long long t0 = PROF_ON ? clk() : 0;
             mbar_wait_cluster(smem_u32(&tempty[acc]), aphase ^ 1u);  // accumulator drained (both CTAs)
+            if (PROF_ON) t_we += clk() - t0;
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
 #pragma unroll 1
-            for (int kb = 0; kb < NB; ++kb) {
+            for (int ks = 0; ks < NST; ++ks) {
+              long long t1 = PROF_ON ? clk() : 0;
               mbar_wait_cluster(smem_u32(&full[mstage]), mphase);      // both halves of B written
+              if (PROF_ON) t_wf += clk() - t1;
               tc_fence_after();
 #pragma unroll
-              for (int ks = 0; ks < KB / 32; ++ks) {
-                const uint64_t ad = smem_desc(a_addr + (uint32_t)(kb * 8 + ks * 2) * A_LBO, A_LBO, SBO);
-                const uint64_t bd = smem_desc(b_addr + (uint32_t)mstage * kStageBytes + (uint32_t)(ks * 2) * B_LBO,
-                                              B_LBO, SBO);
-                mma2_i8(d_tmem, ad, bd, idesc, (kb | ks) != 0 ? 1u : 0u);
+              for (int bb = 0; bb < kBlkPerStage; ++bb) {
+                const int kb = ks * kBlkPerStage + bb;
+                if (kb < NB) {
+#pragma unroll
+                  for (int kk = 0; kk < KB / 32; ++kk) {
+                    const uint64_t ad = smem_desc(a_addr + (uint32_t)(kb * 8 + kk * 2) * A_LBO, A_LBO, SBO);
+                    const uint64_t bd = smem_desc(
+                        b_addr + (uint32_t)mstage * kStageBytes + (uint32_t)(bb * 8 + kk * 2) * B_LBO, B_LBO, SBO);
+                    mma2_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                  }
+                }
               }
               mma2_commit_mc(smem_u32(&empty[mstage]), 0x3);
               if (++mstage == S) { mstage = 0; mphase ^= 1u; }
@@ -225,120 +290,193 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           __syncwarp();
           if (++acc == 2) { acc = 0; aphase ^= 1u; }
         }
+        PROF_ADD(0, clk() - t_loop);
+        PROF_ADD(1, t_we);
+        PROF_ADD(2, t_wf);
+        PROF_ADD(10, 1);
       }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 * kEpiSets) {
-      // ================= epilogue: per-query top-k streams =================
+      // ================= epilogue =================
       // set h handles accumulator columns [h*BN/2, (h+1)*BN/2) of every tile, so
       // each query has kEpiSets streams, each seeing its rows in increasing order
       const int ew = warp - kEpiWarp0;
       const int quarter = ew & 3;             // == warp % 4: TMEM lane quarter
       const int h = ew >> 2;                  // column half
-      const int sidx = h * BM + quarter * 32; // first stream of this warp
-      uint32_t* const wbufs = p.bufs + ((size_t)blockIdx.x * kEpiSets * BM + sidx) * p.cap;
-      uint32_t* const my_buf = wbufs + (size_t)lane * p.cap;
-      uint4* const srow = reinterpret_cast<uint4*>(sEpi + ((size_t)ew * 32 + lane) * 32);
+      const int col = quarter * 32 + lane;    // this thread's query inside the CTA tile
+      const int64_t qme = q0 + col;
       const uint32_t tempty_dst = mapa(smem_u32(&tempty[0]), 0);  // leader's tempty[0]
-      const int64_t qme = q0 + quarter * 32 + lane;
-      int cnt = 0;
-      int thrd = INT32_MIN;  // a score passes iff Delta > thrd
-      if (p.thr0 && qme < p.nq) {
-        const int32_t dk = p.thr0[qme * p.thr0_stride];
-        if (dk != INT32_MIN) thrd = dk - 1;
-      }
       constexpr int CW = BN / kEpiSets;       // columns per set per tile
-      for (int tile = 0; tile < ntiles; ++tile) {
-        mbar_wait(smem_u32(&tfull[acc]), aphase);
-        tc_fence_after();
-        const uint32_t tbase =
-            tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kAccStride) + (uint32_t)(h * CW);
-        const int64_t lr0 = (int64_t)tile * BN + h * CW;  // local row of this set's column 0
-        const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
-        // One 32-column group at a time.  Fast path: 4-score
-        // chunk maxima and one vote.  Slow path (compact code; the fully
-        // unrolled variant thrashed the instruction cache): stage the row in
-        // SMEM, then walk, warp-uniformly, only the chunks where some lane has
-        // a candidate.
-        auto process = [&](uint32_t (&v)[32], int c0) {
-          if (ncols - c0 < 32) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c0 + j >= ncols) v[j] = 0x80000000u;
+      if (MODE == kModeHist) {
+        // Only Delta >= F enters the histogram, F = z nnz(q) / sqrt(d) (z standard
+        // deviations of Delta against unrelated codes, z chosen on the host so
+        // that ~4k unrelated sample rows still clear it): the count above any
+        // bin edge stays a lower bound, and almost every score costs one compare.
+        int floor_m1 = 0x7fffffff;
+        if (qme < p.nq) {
+          const uint8_t* qc = p.q + qme * cb;
+          int nnz = 0;
+          for (int b = 0; b < NB; ++b) {
+            const uint4 a = *reinterpret_cast<const uint4*>(qc + b * 16);
+            const uint4 c = *reinterpret_cast<const uint4*>(qc + pb + b * 16);
+            nnz += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(c.x) + __popc(c.y) +
+                   __popc(c.z) + __popc(c.w);
           }
-          int cm[8];
+          floor_m1 = max(0, (int)(p.zfloor * (float)nnz * rsqrtf((float)p.d))) - 1;
+        }
+        for (int tile = 0; tile < ntiles; ++tile) {
+          mbar_wait(smem_u32(&tfull[acc]), aphase);
+          tc_fence_after();
+          const uint32_t tbase =
+              tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kAccStride) + (uint32_t)(h * CW);
+          const int64_t lr0 = (int64_t)tile * BN + h * CW;
+          const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
+#pragma unroll 1
+          for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + (uint32_t)c0, v);
+            if (ncols - c0 < 32) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
-          const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
-                                      max(cm[6], cm[7]));
-          if (__any_sync(kFull, mx > thrd)) {
-            unsigned cmask = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              srow[i ^ (lane & 7)] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-              cmask |= (cm[i] > thrd ? 1u : 0u) << i;
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j >= ncols) v[j] = 0x80000000u;
             }
-            unsigned wmask = __reduce_or_sync(kFull, cmask);
-            while (wmask) {
-              const int i = __ffs(wmask) - 1;
-              wmask &= wmask - 1;
-              if ((cmask >> i) & 1u) {
-                const uint4 q4 = srow[i ^ (lane & 7)];
-                const uint32_t rb0 = (uint32_t)(lr0 + c0 + 4 * i);
-                if ((int)q4.x > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.x, rb0);
-                if ((int)q4.y > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.y, rb0 + 1);
-                if ((int)q4.z > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.z, rb0 + 2);
-                if ((int)q4.w > thrd) my_buf[cnt++] = local_key(p.kf, (int)q4.w, rb0 + 3);
+            int cm[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
+            const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
+                                        max(cm[6], cm[7]));
+            if (__any_sync(kFull, mx > floor_m1)) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (__any_sync(kFull, cm[i] > floor_m1)) {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const int sc = (int)v[4 * i + j];
+                    if (sc > floor_m1) {
+                      const uint32_t b = min((uint32_t)sc >> p.hshift, (uint32_t)(kHistBins - 1));
+                      atomicAdd(s_hist + (b >> 1) * BM + col, (b & 1u) ? 0x10000u : 1u);
+                    }
+                  }
+                }
               }
             }
-            __syncwarp();
           }
-        };
-#pragma unroll 1
-        for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tbase + (uint32_t)c0, v);
-          process(v, c0);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
+          if (++acc == 2) { acc = 0; aphase ^= 1u; }
+          // the two sets share a u16 counter: flush before 2 * 256 * 96 < 65536 rows accumulate
+          if ((tile & 255) == 255) {
+            named_bar_sync(1 + quarter, 64);  // both sets' warps of this quarter
+            if (h == 0) hist_flush(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBins : nullptr);
+            named_bar_sync(1 + quarter, 64);
+          }
         }
-        tc_fence_before();
+        named_bar_sync(1 + quarter, 64);
+        if (h == 0) hist_flush(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBins : nullptr);
+        named_bar_sync(1 + quarter, 64);
+      } else {
+        const int sidx = h * BM + quarter * 32; // first stream of this warp
+        uint32_t* const wbufs = p.bufs + ((size_t)blockIdx.x * kEpiSets * BM + sidx) * p.cap;
+        uint32_t* const my_buf = wbufs + (size_t)lane * p.cap;
+        int cnt = 0;
+        int thrd = INT32_MIN;  // a score passes iff Delta > thrd
+        if (p.thr0 && qme < p.nq) {
+          const int32_t dk = p.thr0[qme * p.thr0_stride];
+          if (dk != INT32_MIN) thrd = dk - 1;
+        }
+        long long t_loop = PROF_ON ? clk() : 0, t_w = 0, t_f = 0, t_r = 0;
+        for (int tile = 0; tile < ntiles; ++tile) {
+          long long t0 = PROF_ON ? clk() : 0;
+          mbar_wait(smem_u32(&tfull[acc]), aphase);
+          tc_fence_after();
+          long long t1 = PROF_ON ? clk() : 0;
+          if (PROF_ON) t_w += t1 - t0;
+          const uint32_t tbase =
+              tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kAccStride) + (uint32_t)(h * CW);
+          const int64_t lr0 = (int64_t)tile * BN + h * CW;  // local row of this set's column 0
+          const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
+#pragma unroll 1
+          for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + (uint32_t)c0, v);
+            if (ncols - c0 < 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j >= ncols) v[j] = 0x80000000u;
+            }
+            // 4-score maxima, one vote for the whole 32-score row; then, per
+            // 4-score group some lane needs, a register-only append
+            int cm[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
+            const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
+                                        max(cm[6], cm[7]));
+            if (__any_sync(kFull, mx > thrd)) {
+              const uint32_t rb0 = (uint32_t)(lr0 + c0);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (__any_sync(kFull, cm[i] > thrd)) {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const int sc = (int)v[4 * i + j];
+                    if (sc > thrd) my_buf[cnt++] = local_key(p.kf, sc, rb0 + (uint32_t)(4 * i + j));
+                  }
+                }
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
+          if (++acc == 2) { acc = 0; aphase ^= 1u; }
+          long long t2 = PROF_ON ? clk() : 0;
+          if (PROF_ON) t_f += t2 - t1;
+          unsigned need = __ballot_sync(kFull, cnt > p.k + CW);
+          while (need) {
+            const int L = __ffs(need) - 1;
+            need &= need - 1;
+            const int cL = __shfl_sync(kFull, cnt, L);
+            const uint32_t D = ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
+            if (lane == L) {
+              cnt = p.k;
+              thrd = max(thrd, (int)D - p.kf.off);
+            }
+          }
+          if (PROF_ON) t_r += clk() - t2;
+        }
+        long long t_pub = PROF_ON ? clk() : 0;
+        PROF_ADD(5, t_pub - t_loop);
+        PROF_ADD(6, t_w);
+        PROF_ADD(7, t_f);
+        PROF_ADD(8, t_r);
+        // finalize: cut to k, publish global keys as list (chunk, set)
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
-        if (++acc == 2) { acc = 0; aphase ^= 1u; }
-        unsigned need = __ballot_sync(kFull, cnt > p.k + CW);
+        unsigned need = __ballot_sync(kFull, cnt > p.k);
         while (need) {
           const int L = __ffs(need) - 1;
           need &= need - 1;
           const int cL = __shfl_sync(kFull, cnt, L);
-          const uint32_t D = ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
-          if (lane == L) {
-            cnt = p.k;
-            thrd = max(thrd, (int)D - p.kf.off);
-          }
+          ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
+          if (lane == L) cnt = p.k;
         }
-      }
-      // finalize: cut to k, publish global keys as list (chunk, set)
-      __syncwarp();
-      unsigned need = __ballot_sync(kFull, cnt > p.k);
-      while (need) {
-        const int L = __ffs(need) - 1;
-        need &= need - 1;
-        const int cL = __shfl_sync(kFull, cnt, L);
-        ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
-        if (lane == L) cnt = p.k;
-      }
-      __syncwarp();
-      for (int L = 0; L < 32; ++L) {
-        const int64_t qi = q0 + quarter * 32 + L;
-        const int cL = __shfl_sync(kFull, cnt, L);
-        if (qi >= p.nq) continue;
-        const uint32_t* bL = wbufs + (size_t)L * p.cap;
-        uint64_t* out = p.part + ((size_t)(it.c * kEpiSets + h) * p.nq + qi) * p.k;
-        for (int i = lane; i < p.k; i += 32)
-          out[i] = (i < cL) ? global_key_from_local(p.kf, bL[i], (uint64_t)row0) : 0ull;
-        if (it.c == it.s_t - 1)
-          for (int c2 = it.s_t; c2 < p.s_max; ++c2) {
-            uint64_t* z = p.part + ((size_t)(c2 * kEpiSets + h) * p.nq + qi) * p.k;
-            for (int i = lane; i < p.k; i += 32) z[i] = 0ull;
-          }
+        __syncwarp();
+        for (int L = 0; L < 32; ++L) {
+          const int64_t qi = q0 + quarter * 32 + L;
+          const int cL = __shfl_sync(kFull, cnt, L);
+          if (qi >= p.nq) continue;
+          const uint32_t* bL = wbufs + (size_t)L * p.cap;
+          uint64_t* out = p.part + ((size_t)(it.c * kEpiSets + h) * p.nq + qi) * p.k;
+          for (int i = lane; i < p.k; i += 32)
+            out[i] = (i < cL) ? global_key_from_local(p.kf, bL[i], (uint64_t)row0) : 0ull;
+          if (it.c == it.s_t - 1)
+            for (int c2 = it.s_t; c2 < p.s_max; ++c2) {
+              uint64_t* z = p.part + ((size_t)(c2 * kEpiSets + h) * p.nq + qi) * p.k;
+              for (int i = lane; i < p.k; i += 32) z[i] = 0ull;
+            }
+        }
+        PROF_ADD(9, clk() - t_pub);
       }
     }
   }
@@ -350,27 +488,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
   }
 }
 
+// kHist -> per-query seed: thr[q] = (largest b with sum_{b' >= b} hist[q][b'] >= k) << hshift,
+// INT32_MIN if fewer than k sampled rows were counted.  One warp per query
+// (lane l: bins 4l .. 4l+3); clears the histogram.
+__global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, int32_t hshift, int32_t* thr) {
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  uint4* g = reinterpret_cast<uint4*>(ghist + (size_t)q * kHistBins) + lane;
+  const uint4 h = *g;
+  *g = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t tot = h.x + h.y + h.z + h.w;
+  uint32_t suf = tot;  // sum over lanes >= lane
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_down_sync(kFull, suf, o);
+    if (lane + o < 32) suf += t;
+  }
+  // suffix sums of this lane's bins
+  const uint32_t s3 = suf - tot + h.w, s2 = s3 + h.z, s1 = s2 + h.y, s0 = s1 + h.x;
+  const unsigned ok = __ballot_sync(kFull, s0 >= (uint32_t)k);
+  if (ok == 0u) {
+    if (lane == 0) thr[q] = INT32_MIN;
+    return;
+  }
+  const int L = 31 - __clz(ok);
+  if (lane == L) {
+    const int j = (s3 >= (uint32_t)k) ? 3 : (s2 >= (uint32_t)k) ? 2 : (s1 >= (uint32_t)k) ? 1 : 0;
+    thr[q] = (4 * L + j) << hshift;
+  }
+}
+
 }  // namespace tc2
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static int tc2_stages(int NB) {
+static int tc2_stages(int NB, int mode) {
   const int a_bytes = tc2::BM * NB * tc2::KB;
-  const int budget = 227 * 1024 - a_bytes - tc2::kEpiStageWords * 4 - 2048;
+  const int budget = 227 * 1024 - a_bytes - (mode == tc2::kModeHist ? tc2::kHistBytes : 0) - 2048;
   int s = budget / tc2::kStageBytes;
-  if (s > 8) s = 8;
+  if (s > 6) s = 6;
   return s;
+}
+
+static int tc2_hist_shift(int32_t d) {
+  int hs = bitlen((uint32_t)d) - 7;  // (d >> hs) < 128
+  return hs < 0 ? 0 : hs;
 }
 
 // Pairs: the query set is cut into 256-query pair tiles; each of the SMs/2
 // pairs gets one (pair tile, DB chunk) item when the tiles do not cover them.
-TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int mode) {
   TcPlan pl{};
   const int NB = blocks128(d);
   pl.ok = false;
   if (NB > 8 || nq < 1 || n < 1) return pl;
-  pl.stages = tc2_stages(NB);
+  pl.stages = tc2_stages(NB, mode);
   if (pl.stages < 2) return pl;
   pl.ok = true;
   const int npairs = sms / 2;
@@ -396,47 +570,98 @@ TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   pl.n_items = QT * pl.s_lo + pl.r_hi;
   const int64_t pairs = pl.n_items < npairs ? pl.n_items : npairs;
   pl.grid = (int32_t)(2 * pairs);
-  pl.smem = 1024 + tc2::BM * NB * tc2::KB + pl.stages * tc2::kStageBytes + tc2::kEpiStageWords * 4 +
-            (2 * pl.stages + 4) * 8 + 16;
-  pl.buf_bytes = (size_t)pl.grid * tc2::kEpiSets * tc2::BM * pl.cap * 4;
-  pl.part_bytes = (size_t)pl.n_chunks * nq * k * 8;
+  pl.smem = 1024 + tc2::BM * NB * tc2::KB + pl.stages * tc2::kStageBytes +
+            (mode == tc2::kModeHist ? tc2::kHistBytes : 0) + (2 * pl.stages + 4) * 8 + 16;
+  pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * tc2::kEpiSets * tc2::BM * pl.cap * 4;
+  pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * k * 8;
   return pl;
 }
 
-template <int NB>
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  return plan_tc2_mode(nq, n, d, k, sms, tc2::kModeTopK);
+}
+TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  return plan_tc2_mode(nq, n, d, k, sms, tc2::kModeHist);
+}
+
+template <int NB, int MODE>
 static cudaError_t launch_tc2_nb(const tc2::Params& p, const TcPlan& pl, cudaStream_t st) {
-  auto kern = tc2::scan_tc2_kernel<NB>;
+  auto kern = tc2::scan_tc2_kernel<NB, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
   kern<<<pl.grid, tc2::kThreads, pl.smem, st>>>(p);
   note_launch();
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("UQ_DEBUG"))
+    fprintf(stderr, "scan_tc2_kernel<%d,%d> launch (grid %d, smem %d): %s\n", NB, MODE, pl.grid, pl.smem,
+            cudaGetErrorString(e));
+  return e;
+}
+
+template <int MODE>
+static cudaError_t launch_tc2_mode(const tc2::Params& p, const TcPlan& pl, int NB, cudaStream_t st) {
+  switch (NB) {
+    case 1: return launch_tc2_nb<1, MODE>(p, pl, st);
+    case 2: return launch_tc2_nb<2, MODE>(p, pl, st);
+    case 3: return launch_tc2_nb<3, MODE>(p, pl, st);
+    case 4: return launch_tc2_nb<4, MODE>(p, pl, st);
+    case 5: return launch_tc2_nb<5, MODE>(p, pl, st);
+    case 6: return launch_tc2_nb<6, MODE>(p, pl, st);
+    case 7: return launch_tc2_nb<7, MODE>(p, pl, st);
+    case 8: return launch_tc2_nb<8, MODE>(p, pl, st);
+    default: break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+static int tc2_dbg() {
+  static const int dbg = [] {
+    const char* e = getenv("UQ_TC_ABLATE");
+    return e ? atoi(e) : 0;
+  }();
+  return dbg;
+}
+
+// profiling counters (dbg & 8): copy out and reset
+cudaError_t tc2_prof_read(unsigned long long* out16) {
+  cudaError_t e = cudaMemcpyFromSymbol(out16, tc2::g_prof, 16 * sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  static const unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(tc2::g_prof, z, sizeof(z));
 }
 
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                             cudaStream_t st) {
-  const int NB = blocks128(d);
-  static const int dbg = [] {
-    const char* e = getenv("UQ_TC_ABLATE");
-    return e ? atoi(e) : 0;
-  }();
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, bufs, part, thr0, thr0_stride,
-                row_stride, dbg};
-  switch (NB) {
-    case 1: return launch_tc2_nb<1>(p, pl, st);
-    case 2: return launch_tc2_nb<2>(p, pl, st);
-    case 3: return launch_tc2_nb<3>(p, pl, st);
-    case 4: return launch_tc2_nb<4>(p, pl, st);
-    case 5: return launch_tc2_nb<5>(p, pl, st);
-    case 6: return launch_tc2_nb<6>(p, pl, st);
-    case 7: return launch_tc2_nb<7>(p, pl, st);
-    case 8: return launch_tc2_nb<8>(p, pl, st);
-    default: break;
-  }
-  return cudaErrorInvalidValue;
+                row_stride, nullptr, 0, 0.f, tc2_dbg()};
+  return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), st);
+}
+
+// Threshold seeding over rows {i * row_stride : i < n}: histogram scan, then
+// thr[q] (stride 1) from the histogram.  ghist: [nq][128] u32, zero on entry
+// (left zero on exit).
+cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
+                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms,
+                                 cudaStream_t st) {
+  const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms);
+  if (!pl.ok) return cudaErrorInvalidValue;
+  const int hs = tc2_hist_shift(d);
+  // floor: about 4k of n unrelated rows exceed it (Gaussian tail), z in [0, 4]
+  double ptail = 4.0 * (double)k / (double)(n > 0 ? n : 1);
+  if (ptail > 0.5) ptail = 0.5;
+  float z = inv_norm_cdf(1.0 - ptail);
+  z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
+  tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
+                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr, 0,
+                row_stride, ghist, hs, z, tc2_dbg()};
+  cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), st);
+  if (e != cudaSuccess) return e;
+  tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, k, hs, thr);
+  note_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace uq

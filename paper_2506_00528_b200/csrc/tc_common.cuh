@@ -143,6 +143,11 @@ __device__ __forceinline__ void expand_block_store(uint4 p, uint4 n, uint8_t* ba
 }
 
 
+// named barrier over `nthreads` threads (warp multiples) of this CTA
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // Cluster helpers (CTA pairs).
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -62,6 +62,41 @@ def test_encode_parity_shapes(uq, orc, d, dt):
         assert np.array_equal(got, ref), (d, dt, x, np.argwhere((got != ref).any(1))[:5])
 
 
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16, torch.bfloat16])
+def test_encode_extreme_distributions(uq, orc, dt):
+    """Rows the search's probes mis-estimate: subnormal magnitudes, huge dynamic
+    range, heavy tails, constants, all-zero rows, one-hot rows; interleaved so a
+    warp's learned T*/RMS ratio is wrong for the next row (exactness must not
+    depend on the probes)."""
+    rng = np.random.default_rng(11)
+    d, n = 768, 60000
+    kinds = []
+    base = rng.standard_normal((n, d)).astype(np.float32)
+    tiny = 6e-8 if dt == torch.float16 else (1e-39 if dt == torch.float32 else 1e-38)
+    for i in range(n):
+        k = i % 7
+        if k == 1:
+            base[i] *= tiny                                   # subnormal range
+        elif k == 2:
+            base[i] *= np.float32(10.0) ** rng.integers(-4, 4, d)   # wide dynamic range
+        elif k == 3:
+            base[i] = rng.standard_cauchy(d).clip(-6e4, 6e4)  # heavy tails
+        elif k == 4:
+            base[i] = np.float32(rng.integers(-2, 3))         # constant (all ties or zeros)
+        elif k == 5:
+            base[i] = 0.0
+            base[i, rng.integers(0, d)] = -1.0                # one non-zero
+        elif k == 6:
+            base[i] = np.abs(base[i]) + 1.0                   # all magnitudes in [1, ~5]
+    ut = torch.from_numpy(base).to(dt)
+    host = ut.float().numpy()
+    for x in (1, 256, 384, 700, 768):
+        got = uq.encode(ut.cuda(), x).cpu().numpy()
+        ref = orc.pack(orc.encode(host if dt != torch.float16 else ut.numpy(), x))
+        bad = np.argwhere((got != ref).any(1))[:5].ravel()
+        assert bad.size == 0, (dt, x, bad, bad % 7)
+
+
 def test_encode_strided_and_table3(uq, orc):
     import json, os
     t = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table3_p356.json")))

@@ -198,9 +198,147 @@ static void run2(const char* name) {
   cudaFree(cyc);
 }
 
+
+// Pipelined 2-CTA replica of scan_tc2's MMA structure without data work:
+// S stages; per stage the leader waits full[s] (arrivals from one producer warp
+// in each CTA), issues KPS MMAs (M=256, N, K=32), commits to empty[s] in both
+// CTAs; producers wait empty[s] and re-arrive.  ACC=1 adds the per-tile
+// accumulator handshake (tfull / tempty with one epilogue warp per CTA).
+__device__ __forceinline__ bool tryw(uint32_t bar, uint32_t ph) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(ok) : "r"(bar), "r"(ph) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ uint32_t mapa0(uint32_t a) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  return r;
+}
+template <int N, int S, int KPS, int ACC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma3_kernel(int tiles, int ktiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t full[S], empty[S], tfull[2], tempty[2];
+  uint32_t cr;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(cr));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + 128 * 128;
+  for (int i = threadIdx.x; i < (128 + N / 2) * 128 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x01010101u * (i & 1), 0, 0x01010101u, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+    }
+    for (int a = 0; a < 2; ++a) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[a])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(&tempty[a])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s_tmem;
+  const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int total = tiles * ktiles;  // stages
+  if (warp == 1) {        // producer: one warp per CTA
+    int st = 0; uint32_t ph = 0;
+    const uint32_t fdst = mapa0(smem_u32(&full[0]));
+    for (int i = 0; i < total; ++i) {
+      while (!tryw(smem_u32(&empty[st]), ph ^ 1u)) {}
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(fdst + 8u * st) : "memory");
+      if (++st == S) { st = 0; ph ^= 1u; }
+    }
+  } else if (warp == 0 && cr == 0) {   // MMA issuer
+    if (lane == 0) {
+      int st = 0; uint32_t ph = 0; int acc = 0; uint32_t aph = 0;
+      for (int t = 0; t < tiles; ++t) {
+        if (ACC) { while (!tryw(smem_u32(&tempty[acc]), aph ^ 1u)) {} asm volatile("tcgen05.fence::after_thread_sync;"); }
+        for (int kt = 0; kt < ktiles; ++kt) {
+          while (!tryw(smem_u32(&full[st]), ph)) {}
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+          for (int ks = 0; ks < KPS; ++ks) {
+            uint64_t ad = desc(smem_u32(sA) + (ks & 3) * 2 * 128 * 16, 128 * 16, 128, 0);
+            uint64_t bd = desc(smem_u32(sB) + (ks & 3) * 2 * (N / 2) * 16, (N / 2) * 16, 128, 0);
+            uint32_t a = (kt | ks) ? 1u : 0u;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (ACC ? acc * 256 : 0)),
+                         "l"(ad), "l"(bd), "r"(idesc), "r"(a));
+          }
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                       ::"r"(smem_u32(&empty[st])), "h"((uint16_t)3));
+          if (++st == S) { st = 0; ph ^= 1u; }
+        }
+        if (ACC) asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                              ::"r"(smem_u32(&tfull[acc])), "h"((uint16_t)3));
+        if (++acc == 2) { acc = 0; aph ^= 1u; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2 && ACC) {       // epilogue stand-in: release each accumulator
+    int acc = 0; uint32_t aph = 0;
+    const uint32_t tdst = mapa0(smem_u32(&tempty[0]));
+    for (int t = 0; t < tiles; ++t) {
+      while (!tryw(smem_u32(&tfull[acc]), aph)) {}
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tdst + 8u * acc) : "memory");
+      if (++acc == 2) { acc = 0; aph ^= 1u; }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int N, int S, int KPS, int ACC>
+static void run3(const char* name) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int smem = (128 + N / 2) * 128 + 1024;
+  cudaFuncSetAttribute(mma3_kernel<N, S, KPS, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = sms / 2 * 2;
+  const int ktiles = 24 / KPS, tiles = 600;   // K = 768 per tile
+  mma3_kernel<N, S, KPS, ACC><<<grid, 128, smem>>>(4, ktiles);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  mma3_kernel<N, S, KPS, ACC><<<grid, 128, smem>>>(tiles, ktiles);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double macs = (double)(grid / 2) * tiles * 768.0 * 256.0 * N;
+  printf("{\"variant\": \"%s\", \"N\": %d, \"S\": %d, \"mma_per_stage\": %d, \"acc_handshake\": %d, \"err\": \"%s\", \"ms\": %.3f, \"tops\": %.1f}\n",
+         name, N, S, KPS, ACC, cudaGetErrorString(cudaGetLastError()), ms, 2 * macs / (ms * 1e-3) / 1e12);
+}
+
 int main() {
+  run3<192, 8, 4, 0>("pipe");
+  run3<192, 8, 4, 1>("pipe");
+  run3<192, 8, 8, 1>("pipe");
+  run3<192, 4, 8, 1>("pipe");
+  run3<192, 8, 2, 1>("pipe");
+  run3<256, 8, 4, 1>("pipe");
+
   run2<256>("2cta_noswizzle");
   run2<224>("2cta_noswizzle");
+  run2<192>("2cta_noswizzle");
+  run2<128>("2cta_noswizzle");
   run<224, 0>("noswizzle");
   run<224, 2>("sw128");
   run<256, 0>("noswizzle");

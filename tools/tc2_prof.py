@@ -1,0 +1,42 @@
+"""Cycle accounting of the CTA-pair tensor scan (measurement tool): runs
+uq_search on the c2 workload with UQ_TC_ABLATE=8 (instrumented, results
+unchanged) and prints where each warp role spends its cycles."""
+import ctypes
+import json
+import os
+import sys
+
+os.environ["UQ_TC_ABLATE"] = str(int(os.environ.get("UQ_TC_ABLATE", "0")) | 8)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+import paper_2506_00528_b200 as uq  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else None
+nq = int(sys.argv[3]) if len(sys.argv) > 3 else None
+w = datagen.CONFIGS[cfg].scaled(n=n, nq=nq)
+db = uq.encode(datagen.db(w, "cuda"), w.x)
+q = uq.encode(datagen.queries(w, "cuda"), w.x)
+ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, uq.ALGO_TCGEN05), dtype=torch.uint8, device="cuda")
+L = uq._L
+L.uq_debug_tc2_prof.argtypes = [ctypes.c_void_p]
+buf = (ctypes.c_ulonglong * 16)()
+for _ in range(2):
+    uq.search(q, db, w.d, w.k, algo=uq.ALGO_TCGEN05, workspace=ws)
+torch.cuda.synchronize()
+L.uq_debug_tc2_prof(buf)  # reset
+reps = 5
+for _ in range(reps):
+    uq.search(q, db, w.d, w.k, algo=uq.ALGO_TCGEN05, workspace=ws)
+torch.cuda.synchronize()
+L.uq_debug_tc2_prof(buf)
+c = list(buf)
+out = {"cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
+       "mma_wait_tempty_frac": c[1] / max(c[0], 1), "mma_wait_full_frac": c[2] / max(c[0], 1),
+       "prod_wait_empty_frac": c[4] / max(c[3], 1),
+       "epi_wait_tfull_frac": c[6] / max(c[5], 1), "epi_filter_frac": c[7] / max(c[5], 1),
+       "epi_rebuild_frac": c[8] / max(c[5], 1), "epi_publish_over_loop": c[9] / max(c[5], 1),
+       "mma_loop_cycles_per_item": c[0] / max(c[10], 1), "raw": c}
+print(json.dumps(out))
