@@ -203,31 +203,34 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
       }
     } else if (warp == kMmaWarp) {
       // ================= MMA issuer =================
+      // warp-uniform loop (descriptors in uniform registers), one elected lane
+      // issues each tcgen05 instruction
       constexpr uint32_t idesc = idesc_i8(BM, BN);
-      const uint32_t a_addr = smem_u32(sA);
-      const uint32_t b_addr = smem_u32(sB);
+      const uint64_t a_desc0 = smem_desc(smem_u32(sA), A_LBO, SBO);
+      const uint64_t b_desc0 = smem_desc(smem_u32(sB), B_LBO, SBO);
       for (int tile = 0; tile < ntiles; ++tile) {
-        if (lane == 0) {
-          mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1u);
-          tc_fence_after();
-          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
+        mbar_wait(smem_u32(&tempty[acc]), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
 #pragma unroll 1
-          for (int kb = 0; kb < NB; ++kb) {
-            mbar_wait(smem_u32(&full[stage]), sphase);
-            tc_fence_after();
+        for (int kb = 0; kb < NB; ++kb) {
+          mbar_wait(smem_u32(&full[stage]), sphase);
+          tc_fence_after();
+          const uint64_t b_stage = b_desc0 + (uint64_t)(((uint32_t)stage * kStageBytes) >> 4);
+          const uint64_t a_blk = a_desc0 + (uint64_t)(((uint32_t)(kb * 8) * A_LBO) >> 4);
+          if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < KB / 32; ++ks) {
-              const uint64_t ad = smem_desc(a_addr + (uint32_t)(kb * 8 + ks * 2) * A_LBO, A_LBO, SBO);
-              const uint64_t bd = smem_desc(b_addr + (uint32_t)stage * kStageBytes + (uint32_t)(ks * 2) * B_LBO,
-                                            B_LBO, SBO);
+              const uint64_t ad = a_blk + (uint64_t)(((uint32_t)(ks * 2) * A_LBO) >> 4);
+              const uint64_t bd = b_stage + (uint64_t)(((uint32_t)(ks * 2) * B_LBO) >> 4);
               mma_i8(d_tmem, ad, bd, idesc, (kb | ks) != 0 ? 1u : 0u);
             }
             mma_commit(smem_u32(&empty[stage]));
-            if (++stage == S) { stage = 0; sphase ^= 1u; }
+            if (kb == NB - 1) mma_commit(smem_u32(&tfull[acc]));
           }
-          mma_commit(smem_u32(&tfull[acc]));
+          __syncwarp();
+          if (++stage == S) { stage = 0; sphase ^= 1u; }
         }
-        __syncwarp();
         if (++acc == 2) { acc = 0; aphase ^= 1u; }
       }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {

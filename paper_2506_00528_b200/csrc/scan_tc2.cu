@@ -3,12 +3,12 @@
 //
 // Same contraction as scan_tc.cu (Delta = T_q . T_db^T over {-1,0,1}, s32,
 // exact; P:209-216 / P:385-389) on a 2-CTA cluster: the pair computes a
-// 256-query x 192-row tile.  CTA r of the pair
+// 256-query x 256-row tile.  CTA r of the pair
 //   * keeps its own 128 queries resident in SMEM (A, 128 x 128*NB int8),
-//   * expands only rows [96 r, 96 r + 96) of each 192-row DB tile (its half
+//   * expands only rows [128 r, 128 r + 128) of each 256-row DB tile (its half
 //     of B), so each SM expands half as many DB rows per unit of MMA work as
 //     the one-CTA kernel -- the expansion is the per-SM instruction bottleneck,
-//   * holds the 128 x 192 s32 accumulator of its own queries in TMEM (two
+//   * holds the 128 x 256 s32 accumulator of its own queries in TMEM (two
 //     buffers) and runs their epilogue in its epilogue warps.
 // A pipeline stage carries 256 dims (two 128-dim blocks, 8 MMAs of K=32): the
 // per-stage barrier round trip (producers of both CTAs -> leader `full`, MMA
@@ -25,11 +25,13 @@
 //          histogram; F ~ 2 sigma of unrelated-code Delta filters ~98% first).  At least sum_{b' >= b} hist[b'] rows have Delta >=
 //          b << hshift, so thr_from_hist_kernel's per-query bound is exact.
 //
-// Warps: 0-2 producers (one thread per DB row of this CTA's 96-row half),
-// 3 MMA issuer (leader) + TMEM owner, 4-11 epilogue in two sets of four
-// (warp % 4 = TMEM lane quarter; set h reads accumulator columns
-// [96 h, 96 h + 96)).  12 warps = 3 per SM sub-partition, whose 16K-register
-// file then allows 168 registers per thread (a 13th warp would cap it at 128).
+// Warps: 0-3 producers (one thread per DB row of this CTA's 128-row half; the
+// int8 expansion is bound by the integer ALU pipe of each SM sub-partition, so
+// one producer warp per sub-partition), warp 3 of the leader also issues the
+// MMAs, 4-11 epilogue in two sets of four (warp % 4 = TMEM lane quarter; set h
+// reads accumulator columns [128 h, 128 h + 128)).  12 warps = 3 per SM
+// sub-partition, whose 16K-register file allows 168 registers per thread (a
+// 13th warp would cap it at 128).
 #include <cstdio>
 #include <cstdlib>
 
@@ -43,18 +45,18 @@ namespace tc2 {
 using namespace ::uq::tc;
 
 constexpr int BM = 128;               // queries per CTA (pair M = 256)
-constexpr int BN = 192;               // DB rows per pair tile (UMMA N)
-constexpr int BH = BN / 2;            // DB rows expanded per CTA (96: three producer warps)
+constexpr int BN = 256;               // DB rows per pair tile (UMMA N)
+constexpr int BH = BN / 2;            // DB rows expanded per CTA (128: four producer warps)
 constexpr int KB = 128;               // dims per expansion block (one uint4 of each plane)
 constexpr int kBlkPerStage = 2;       // 256 dims per pipeline stage
-constexpr int kProdWarps = 3;         // warps 0-2
-constexpr int kMmaWarp = 3;           // warp 3: MMA issuer (leader) + TMEM owner
+constexpr int kProdWarps = 4;         // warps 0-3
+constexpr int kMmaWarp = 3;           // warp 3: also MMA issuer (leader) + TMEM owner
 constexpr int kEpiSets = 2;           // epilogue warp sets, each owns half of a tile's columns
 constexpr int kEpiWarp0 = 4;          // warps 4..11 (warp % 4 = TMEM lane quarter)
-constexpr int kThreads = (4 + 4 * kEpiSets) * 32;  // 12 warps: 3 per SMSP -> 168 regs
+constexpr int kThreads = (kProdWarps + 4 * kEpiSets) * 32;  // 12 warps: 3 per SMSP -> 168 regs
 constexpr int kAccStride = 256;       // TMEM column offset of the second accumulator
-constexpr int kBlkBytes = BH * KB;    // 12 KB per CTA per 128-dim block
-constexpr int kStageBytes = kBlkPerStage * kBlkBytes;  // 24 KB
+constexpr int kBlkBytes = BH * KB;    // 16 KB per CTA per 128-dim block
+constexpr int kStageBytes = kBlkPerStage * kBlkBytes;  // 32 KB
 constexpr uint32_t kTmemCols = 512;   // two s32 accumulators (columns 0 and 256)
 constexpr int kHistBins = 128;
 constexpr int kHistBytes = (kHistBins / 2) * BM * 4;   // [64 words][128 queries], two u16 counts per word
@@ -81,7 +83,8 @@ struct Params {
   uint32_t* ghist;      // kHist: [nq][kHistBins]
   int32_t hshift;       // kHist: bin = Delta >> hshift
   float zfloor;         // kHist: only Delta >= zfloor * nnz(q) / sqrt(d) is counted
-  int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads
+  int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads,
+                        // 8 cycle accounting, 16 no producer proxy fence
 };
 
 // Cycle accounting (ablation/profiling only: dbg & 8), read by uq_tc2_prof:
@@ -208,7 +211,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
     cluster_sync();  // both CTAs' A tiles are in place before the leader issues
 
     if (warp < kProdWarps) {
-      // ================= producers: rows [cr*96, cr*96+96) of each tile =================
+      // ================= producers: rows [cr*BH, cr*BH+BH) of each tile =================
+      // Warp kMmaWarp of the leader CTA is also the MMA issuer: after writing
+      // its rows of a stage it waits for the pair's `full` barrier and issues
+      // the stage's 8 MMAs (warp-uniform loop, one elected lane), so every SM
+      // sub-partition carries one producer warp and the issue costs only a few
+      // uniform-datapath instructions per stage.
+      const bool issuer = leader && warp == kMmaWarp;
       const int r = threadIdx.x;
       const uint32_t full_dst = mapa(smem_u32(&full[0]), 0);  // leader's full[0]
       uint4 dp[NB], dn[NB];
@@ -225,8 +234,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       };
 #pragma unroll
       for (int kb = 0; kb < NB; ++kb) load_block(0, kb, dp[kb], dn[kb]);
-      long long t_loop = PROF_ON ? clk() : 0, t_wait = 0;
+      long long t_loop = PROF_ON ? clk() : 0, t_wait = 0, t_we = 0, t_wf = 0;
+      // L2 prefetch of this warp's 32 rows two tiles ahead (contiguous rows only):
+      // the register ring hides one tile of latency, L2 covers the rest
+      auto prefetch_rows = [&](int tile) {
+        const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + (r & ~31);
+        if (p.row_stride == 1 && lane == 0 && tile < ntiles && lr < rows) {
+          const int64_t nr = (rows - lr < 32) ? rows - lr : 32;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.db + (row0 + lr) * cb),
+                       "r"((uint32_t)(nr * cb)) : "memory");
+        }
+      };
+      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      const uint64_t a_desc0 = smem_desc(smem_u32(sA), A_LBO, SBO);
+      const uint64_t b_desc0 = smem_desc(smem_u32(sB), B_LBO, SBO);
+      prefetch_rows(1);
       for (int tile = 0; tile < ntiles; ++tile) {
+        prefetch_rows(tile + 2);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
 #pragma unroll
         for (int ks = 0; ks < NST; ++ks) {
           long long t0 = PROF_ON ? clk() : 0;
@@ -241,55 +266,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
               load_block(tile + 1, kb, dp[kb], dn[kb]);
             }
           }
-          fence_proxy_async();
+          if (!(p.dbg & 16)) fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(full_dst + (uint32_t)stage * 8u);
-          if (++stage == S) { stage = 0; sphase ^= 1u; }
-        }
-      }
-      PROF_ADD(3, clk() - t_loop);
-      PROF_ADD(4, t_wait);
-    } else if (warp == kMmaWarp) {
-      // ================= MMA issuer (leader CTA, one lane) =================
-      if (leader) {
-        constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
-        const uint32_t a_addr = smem_u32(sA);
-        const uint32_t b_addr = smem_u32(sB);
-        long long t_loop = PROF_ON ? clk() : 0, t_we = 0, t_wf = 0;
-        for (int tile = 0; tile < ntiles; ++tile) {
-          if (lane == 0) {
-            long long t0 = PROF_ON ? clk() : 0;
-            mbar_wait_cluster(smem_u32(&tempty[acc]), aphase ^ 1u);  // accumulator drained (both CTAs)
-            if (PROF_ON) t_we += clk() - t0;
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
-#pragma unroll 1
-            for (int ks = 0; ks < NST; ++ks) {
+          if (issuer) {
+            if (ks == 0) {
               long long t1 = PROF_ON ? clk() : 0;
-              mbar_wait_cluster(smem_u32(&full[mstage]), mphase);      // both halves of B written
-              if (PROF_ON) t_wf += clk() - t1;
-              tc_fence_after();
+              mbar_wait_cluster(smem_u32(&tempty[acc]), aphase ^ 1u);  // accumulator drained (both CTAs)
+              if (PROF_ON) t_we += clk() - t1;
+            }
+            long long t2 = PROF_ON ? clk() : 0;
+            mbar_wait_cluster(smem_u32(&full[stage]), sphase);       // all rows of the stage written
+            tc_fence_after();
+            if (PROF_ON) t_wf += clk() - t2;
+            const uint64_t b_stage = b_desc0 + (uint64_t)(((uint32_t)stage * kStageBytes) >> 4);
+            if (elect_one()) {
 #pragma unroll
               for (int bb = 0; bb < kBlkPerStage; ++bb) {
                 const int kb = ks * kBlkPerStage + bb;
                 if (kb < NB) {
 #pragma unroll
                   for (int kk = 0; kk < KB / 32; ++kk) {
-                    const uint64_t ad = smem_desc(a_addr + (uint32_t)(kb * 8 + kk * 2) * A_LBO, A_LBO, SBO);
-                    const uint64_t bd = smem_desc(
-                        b_addr + (uint32_t)mstage * kStageBytes + (uint32_t)(bb * 8 + kk * 2) * B_LBO, B_LBO, SBO);
+                    const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)(kb * 8 + kk * 2) * A_LBO) >> 4);
+                    const uint64_t bd = b_stage + (uint64_t)(((uint32_t)(bb * 8 + kk * 2) * B_LBO) >> 4);
                     mma2_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                   }
                 }
               }
-              mma2_commit_mc(smem_u32(&empty[mstage]), 0x3);
-              if (++mstage == S) { mstage = 0; mphase ^= 1u; }
+              mma2_commit_mc(smem_u32(&empty[stage]), 0x3);
+              if (ks == NST - 1) mma2_commit_mc(smem_u32(&tfull[acc]), 0x3);
             }
-            mma2_commit_mc(smem_u32(&tfull[acc]), 0x3);
+            __syncwarp();
           }
-          __syncwarp();
-          if (++acc == 2) { acc = 0; aphase ^= 1u; }
+          if (++stage == S) { stage = 0; sphase ^= 1u; }
         }
+        if (++acc == 2) { acc = 0; aphase ^= 1u; }
+      }
+      PROF_ADD(3, clk() - t_loop);
+      PROF_ADD(4, t_wait);
+      if (issuer) {
         PROF_ADD(0, clk() - t_loop);
         PROF_ADD(1, t_we);
         PROF_ADD(2, t_wf);
@@ -365,8 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
           if (++acc == 2) { acc = 0; aphase ^= 1u; }
-          // the two sets share a u16 counter: flush before 2 * 256 * 96 < 65536 rows accumulate
-          if ((tile & 255) == 255) {
+          // u16 counters: flush every 128 tiles (128 * 256 rows < 65536 per query)
+          if ((tile & 127) == 127) {
             named_bar_sync(1 + quarter, 64);  // both sets' warps of this quarter
             if (h == 0) hist_flush(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBins : nullptr);
             named_bar_sync(1 + quarter, 64);
@@ -406,7 +421,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
                 if (c0 + j >= ncols) v[j] = 0x80000000u;
             }
             // 4-score maxima, one vote for the whole 32-score row; then, per
-            // 4-score group some lane needs, a register-only append
+            // 4-score chunk some lane needs, a register-only append
             int cm[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)

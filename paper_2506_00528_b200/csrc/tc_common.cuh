@@ -83,6 +83,17 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[3
       : "r"(taddr));
   }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait::ld that the compiler sees as defining v (uses of v stay after it)
+__device__ __forceinline__ void tmem_wait_ld_dep(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -119,6 +130,7 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 }
 
 // 32 dims (one 32-bit word of each plane) -> 8 words of int8 in K-permuted order.
+// (Moving half the shifts to the FMA pipe as IMAD.HI measured slower.)
 __device__ __forceinline__ void expand_word(uint32_t p, uint32_t n, uint32_t (&o)[8]) {
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
@@ -128,20 +140,33 @@ __device__ __forceinline__ void expand_word(uint32_t p, uint32_t n, uint32_t (&o
   }
 }
 
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 // One 128-dim block (uint4 of each plane) of one row -> 8 chunks of 16 B at
-// chunk addresses base + c * chunk_stride (c = 0..7).
+// chunk addresses base + c * chunk_stride (c = 0..7).  Explicit st.shared
+// (a generic store would be translated per access).
 __device__ __forceinline__ void expand_block_store(uint4 p, uint4 n, uint8_t* base, uint32_t chunk_stride) {
   const uint32_t pw[4] = {p.x, p.y, p.z, p.w};
   const uint32_t nw[4] = {n.x, n.y, n.z, n.w};
+  const uint32_t sbase = smem_u32(base);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     uint32_t o[8];
     expand_word(pw[w], nw[w], o);
-    *reinterpret_cast<uint4*>(base + (2 * w) * chunk_stride) = make_uint4(o[0], o[1], o[2], o[3]);
-    *reinterpret_cast<uint4*>(base + (2 * w + 1) * chunk_stride) = make_uint4(o[4], o[5], o[6], o[7]);
+    st_shared_v4(sbase + (2 * w) * chunk_stride, o[0], o[1], o[2], o[3]);
+    st_shared_v4(sbase + (2 * w + 1) * chunk_stride, o[4], o[5], o[6], o[7]);
   }
 }
 
+
+// one lane of the (converged) warp returns true
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 
 // named barrier over `nthreads` threads (warp multiples) of this CTA
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
