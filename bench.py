@@ -47,6 +47,18 @@ def _peaks():
             "sm_max_mhz": 1965.0}, "fallback"
 
 
+def _traffic(algo: str, workload: str, nq: int):
+    """DRAM bytes per main-scan launch from a committed ncu capture (profiles/traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        e = t.get(f"{algo}/{workload}/{nq}")
+        return (float(e["bytes"]), e["source"]) if e else (None, None)
+    except Exception:
+        return None, None
+
+
 def _popc_peak():
     """POPC/clk/SM measured by tools/peaks.cu on a B200 (profiles/peaks_r01.json)."""
     p = os.path.join(ROOT, "profiles", "peaks_r01.json")
@@ -342,6 +354,9 @@ def main():
                     "kernel": "scan_popc_kernel (LOP3+POPC Delta scan + fused top-k)",
                     "peak_source": f"{popc_clk:.2f} POPC/clk/SM {popc_src} x {sms} SMs x {sm_mhz:.0f} MHz",
                     "algorithmic": "2*ceil(d/32) POPC per Delta"}
+    roof["traffic"], tsrc = _traffic("tcgen05" if used_tc else "popc", w.name, nq)
+    if tsrc:
+        roof["traffic_source"] = tsrc
     roof["scan_ms_avg"] = scan_avg_s * 1e3
     roof["scan_share_of_step"] = (main_ms / max(ms, 1e-9)) if world == 1 else None
     roof["seed_scan"] = {"ms_avg": seed_ms / max(seed_n, 1), "launches": seed_n,
