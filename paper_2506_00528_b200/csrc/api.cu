@@ -66,9 +66,9 @@ static uq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? UQ_OK : UQ
 
 // The tensor-core engine runs on CTA pairs (cta_group::2) once the query
 // batch fills a 256-query pair tile; smaller batches use the one-CTA kernel.
-static bool use_pairs(int64_t nq) { return nq > 128; }
+static bool use_pairs(int64_t nq, int32_t d) { return nq > 128 && blocks128(d) <= 8; }
 static TcPlan plan_tc_any(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  return use_pairs(nq) ? plan_tc2(nq, n, d, k, sms) : plan_tc(nq, n, d, k, sms);
+  return use_pairs(nq, d) ? plan_tc2(nq, n, d, k, sms) : plan_tc(nq, n, d, k, sms);
 }
 
 // Which scan engine runs for a shape.
@@ -78,7 +78,9 @@ static uq_algo resolve_algo(uq_algo algo, int64_t nq, int64_t n, int32_t d, int3
   if (algo == UQ_ALGO_TCGEN05) return tp.ok ? UQ_ALGO_TCGEN05 : UQ_ALGO_AUTO /* unsupported */;
   // AUTO: the popcount scan is POPC-issue-bound once nq exceeds ~3 (DESIGN.md
   // roofline); the int8 tensor path wins for query batches that fill an M tile.
-  if (tp.ok && nq >= 64) return UQ_ALGO_TCGEN05;
+  // small databases: the tensor engines' fixed per-CTA cost (TMEM allocation,
+  // query-tile expansion, pipeline fill) exceeds a popcount scan of few rows
+  if (tp.ok && nq >= 64 && n >= ((int64_t)1 << 16)) return UQ_ALGO_TCGEN05;
   return UQ_ALGO_POPC;
 }
 
@@ -105,14 +107,17 @@ struct SeedPlan {
 };
 // Histogram seeding (CTA-pair tensor engine): a cheap epilogue, so a denser
 // sample (1/8) buys a tighter bound.  Top-k seeding (other engines): 1/32.
-static bool hist_seed(uq_algo a, int64_t nq) { return a == UQ_ALGO_TCGEN05 && use_pairs(nq); }
+static bool hist_seed(uq_algo a, int64_t nq, int32_t d) { return a == UQ_ALGO_TCGEN05 && use_pairs(nq, d); }
 static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
   SeedPlan sp{false, 0, 1};
   static const int div_env = [] {
     const char* e = getenv("UQ_SEED_DIV");  // experiment knob: 0 disables seeding
     return e ? atoi(e) : -1;
   }();
-  const int seed_div = div_env >= 0 ? div_env : (hist ? 8 : 32);
+  int seed_div = div_env >= 0 ? div_env : (hist ? 8 : 32);
+  // large databases: ~512k sampled rows already bound D_k tightly for the
+  // configs' k (c5: 5e7 rows, k = 10); more only lengthens the seeding scan
+  if (div_env < 0 && n / seed_div > ((int64_t)1 << 19) && (int64_t)k <= 256) seed_div = (int)(n >> 19);
   if (seed_div <= 0) return sp;
   if (n < (int64_t)1 << 16) return sp;
   int64_t rows = n / seed_div;
@@ -143,7 +148,7 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   SearchLayout L{0, 0, 0, 0, 0, 0};
   if (nq == 0 || n == 0) return L;
   size_t bufs = 0, part = engine_bytes(a, nq, n, d, k, sms, &bufs);
-  const bool hist = hist_seed(a, nq);
+  const bool hist = hist_seed(a, nq, d);
   const SeedPlan sp = plan_seed(n, k, hist);
   if (sp.on && !hist) {
     size_t b2 = 0, p2 = engine_bytes(a, nq, sp.rows, d, k, sms, &b2);
@@ -175,7 +180,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   timer_begin(st, &ev, timer_kind, (double)nq * (double)n);
   if (a == UQ_ALGO_TCGEN05) {
     const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
-    e = use_pairs(nq) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st)
+    e = use_pairs(nq, d) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st)
                       : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
     lists = tp.n_chunks;
   } else {
@@ -322,7 +327,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   const SearchLayout L = layout_for(a, nq, n, d, k, sms);
   uint32_t* bufs = reinterpret_cast<uint32_t*>(ws + L.bufs_off);
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part_off);
-  const bool hist = hist_seed(a, nq);
+  const bool hist = hist_seed(a, nq, d);
   const SeedPlan sp = plan_seed(n, k, hist);
   const int32_t* thr0 = nullptr;
   int32_t thr0_stride = k;

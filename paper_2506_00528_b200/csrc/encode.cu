@@ -29,6 +29,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -166,6 +168,18 @@ struct Counter<__half, E, NCH> {
 
 #define KEY(e) raw_elem<T>(raw[(e) / VEC], (e) % VEC)
 
+// Four words of 16-bit lanes with flags in bits 15 and 31 -> 8 bits, bit
+// 2i + h = flag of half h of word i (PRMT gathers the flag bytes, one multiply
+// moves bits 7/15/23/31 to 28..31 without carries).
+__device__ __forceinline__ uint32_t flags16_to_bits8(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
+  const uint32_t t01 = __byte_perm(w0, w1, 0x7531);
+  const uint32_t t23 = __byte_perm(w2, w3, 0x7531);
+  const uint32_t n01 = ((t01 & 0x80808080u) * 0x00204081u) >> 28;
+  const uint32_t n23 = ((t23 & 0x80808080u) * 0x00204081u) >> 28;
+  return n01 | (n23 << 4);
+}
+__device__ __forceinline__ __half2 as_h2(uint32_t w) { return *reinterpret_cast<const __half2*>(&w); }
+
 // NCH: chunks of 32*VEC elements per row (compile-time so keys live in registers).
 template <typename T, int NCH, bool VECLOAD>
 __global__ void __launch_bounds__(kEncWarps * 32)
@@ -205,21 +219,42 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
     // ---- keys, sign bits, RMS estimate (element e of lane: chunk e/VEC, offset e%VEC) ----
     uint64_t sgnm = 0;   // sign bits of this lane's elements (bit e; E <= 64)
     float ss = 0.f;
+    if constexpr (std::is_same<T, __half>::value) {
+      // sign flags are bits 15/31 of each word; RMS from HFMA2 on pre-scaled
+      // halves (an estimate: overflow only degrades the probes)
+      __half2 acc = __float2half2_rn(0.f);
+      const __half2 sc = __float2half2_rn(0.015625f);
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) {
-        const uint32_t r = raw_elem<T>(raw[j], c);
-        const int e = j * VEC + c;
-        if (EB::sign(r)) sgnm |= 1ull << e;
+      for (int j = 0; j < NCH; ++j) {
+        sgnm |= (uint64_t)flags16_to_bits8(raw[j].x, raw[j].y, raw[j].z, raw[j].w) << (8 * j);
         if (j < NS) {
-          const float v = EB::key2f(EB::abs_bits(r));
-          ss = fmaf(v, v, ss);
+          const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const __half2 h = __hmul2(as_h2(w[i]), sc);
+            acc = __hfma2(h, h, acc);
+          }
         }
+        raw[j].x &= 0x7fff7fffu; raw[j].y &= 0x7fff7fffu; raw[j].z &= 0x7fff7fffu; raw[j].w &= 0x7fff7fffu;
       }
-      // keys in place: clear the sign bits
-      constexpr uint32_t m = (sizeof(T) == 4) ? 0x7fffffffu : 0x7fff7fffu;
-      raw[j].x &= m; raw[j].y &= m; raw[j].z &= m; raw[j].w &= m;
+      ss = (__low2float(acc) + __high2float(acc)) * 4096.f;
+    } else {
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          const uint32_t r = raw_elem<T>(raw[j], c);
+          const int e = j * VEC + c;
+          if (EB::sign(r)) sgnm |= 1ull << e;
+          if (j < NS) {
+            const float v = EB::key2f(EB::abs_bits(r));
+            ss = fmaf(v, v, ss);
+          }
+        }
+        // keys in place: clear the sign bits
+        constexpr uint32_t m = (sizeof(T) == 4) ? 0x7fffffffu : 0x7fff7fffu;
+        raw[j].x &= m; raw[j].y &= m; raw[j].z &= m; raw[j].w &= m;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
@@ -279,9 +314,19 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
       // non-zero magnitudes -> every non-zero is selected; selected zeros
       // would encode as 0 anyway (R2), so they need no bit.
       const uint32_t lo_sel = (Tk == 0) ? 1u : Tk;
+      if constexpr (std::is_same<T, __half>::value) {
+        const __half hs = __ushort_as_half((unsigned short)lo_sel);
+        const __half2 t2 = __halves2half2(hs, hs);
 #pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (KEY(e) >= lo_sel) selm |= 1ull << e;
+        for (int j = 0; j < NCH; ++j)
+          selm |= (uint64_t)flags16_to_bits8(__hge2_mask(as_h2(raw[j].x), t2), __hge2_mask(as_h2(raw[j].y), t2),
+                                             __hge2_mask(as_h2(raw[j].z), t2), __hge2_mask(as_h2(raw[j].w), t2))
+                  << (8 * j);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (KEY(e) >= lo_sel) selm |= 1ull << e;
+      }
     } else {
       int cgt = 0;
 #pragma unroll

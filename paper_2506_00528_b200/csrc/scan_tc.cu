@@ -34,16 +34,23 @@ namespace uq {
 namespace tc {
 
 constexpr int BM = 128;              // queries per tile (UMMA M, TMEM lanes)
-constexpr int BN = 224;              // DB rows per tile (UMMA N, accumulator columns)
 constexpr int KB = 128;              // K bytes (= dims) per pipeline stage
-constexpr int kProdWarps = 7;        // one producer thread per DB row of the tile
-constexpr int kMmaWarp = 7;
-constexpr int kEpiWarp0 = 8;         // warps 8..11 (warp % 4 = TMEM lane quarter)
-constexpr int kThreads = 12 * 32;    // 3 warps per SM sub-partition -> 168 regs/thread
 constexpr int kAccStride = 256;      // TMEM column offset of the second accumulator
-constexpr int kStageBytes = BN * KB; // 28 KB
 constexpr uint32_t kTmemCols = 512;
-constexpr int kEpiStageWords = 4 * 32 * 32;  // epilogue: one 32-score row per thread
+constexpr int kBnWide = 224;         // DB rows per tile (UMMA N) for d <= 1024
+constexpr int kBnNarrow = 64;        // d in (1024, 1536]: the 192 KB query tile leaves room for 8 KB stages only
+
+// Per-N layout: one producer thread per DB row of the tile; warp kMmaWarp
+// issues the MMAs; four epilogue warps start at a multiple of 4 (warp % 4 =
+// TMEM lane quarter).  N = 224: 12 warps (168 registers); N = 64: 8 warps.
+template <int BN>
+struct Cfg {
+  static constexpr int kProdWarps = BN / 32;
+  static constexpr int kMmaWarp = kProdWarps;
+  static constexpr int kEpiWarp0 = (kProdWarps + 1 + 3) / 4 * 4;
+  static constexpr int kThreads = (kEpiWarp0 + 4) * 32;
+  static constexpr int kStageBytes = BN * KB;
+};
 
 struct Params {
   const uint8_t* q;
@@ -75,6 +82,7 @@ struct Item {
   int64_t row0, rows;
 };
 
+template <int BN>
 __device__ __forceinline__ Item decode_item(const Params& p, int64_t i, int64_t n) {
   Item it;
   const int64_t big = (int64_t)p.r_hi * (p.s_lo + 1);
@@ -98,17 +106,18 @@ __device__ __forceinline__ Item decode_item(const Params& p, int64_t i, int64_t 
 }
 
 // ---------------------------------------------------------------------------
-template <int NB>
-__global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
+template <int NB, int BN>
+__global__ void __launch_bounds__(Cfg<BN>::kThreads, 1) scan_tc_kernel(Params p) {
+  constexpr int kProdWarps = Cfg<BN>::kProdWarps, kMmaWarp = Cfg<BN>::kMmaWarp, kEpiWarp0 = Cfg<BN>::kEpiWarp0;
+  constexpr int kThreads = Cfg<BN>::kThreads, kStageBytes = Cfg<BN>::kStageBytes;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int KTOT = NB * KB;                 // K bytes of the A tile
   constexpr uint32_t A_LBO = BM * 16;           // 2048: next 16-B K chunk
-  constexpr uint32_t B_LBO = BN * 16;           // 3584
+  constexpr uint32_t B_LBO = BN * 16;           // next 16-B K chunk of B
   constexpr uint32_t SBO = 128;                 // next 8-row group
   uint8_t* sA = smem;                                        // [KTOT/16][BM/8][8][16]
   uint8_t* sB = smem + (size_t)BM * KTOT;                    // stages x [8][BN/8][8][16]
-  uint32_t* sEpi = reinterpret_cast<uint32_t*>(sB + (size_t)p.stages * kStageBytes);  // [4][32][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiStageWords);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * kStageBytes);
   uint64_t* full = bars;                  // [stages]  producers -> MMA (count 256)
   uint64_t* empty = bars + p.stages;      // [stages]  MMA commit -> producers
   uint64_t* tfull = bars + 2 * p.stages;  // [2]       MMA commit -> epilogue
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
   uint32_t* my_buf = p.bufs + ((size_t)blockIdx.x * BM + (eq >= 0 ? eq : 0)) * p.cap;
 
   for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-    const Item it = decode_item(p, item, p.n);
+    const Item it = decode_item<BN>(p, item, p.n);
     const int64_t q0 = (int64_t)it.t * BM;
     const int64_t row0 = it.row0;
     const int64_t rows = it.rows;
@@ -242,8 +251,6 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
         const int32_t dk = p.thr0[(q0 + eq) * p.thr0_stride];
         if (dk != INT32_MIN) thrd = dk - 1;  // pass iff Delta >= D_k
       }
-      // this lane's 32-score staging row (16-B chunks XOR-swizzled by lane)
-      uint4* srow = reinterpret_cast<uint4*>(sEpi + (quarter * 32 + lane) * 32);
       for (int tile = 0; tile < ntiles; ++tile) {
         mbar_wait(smem_u32(&tfull[acc]), aphase);
         tc_fence_after();
@@ -259,7 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
             for (int j = 0; j < 32; ++j)
               if (c0 + j >= ncols) v[j] = 0x80000000u;
           }
-          // per 4-score chunk maxima, then the lane maximum (3-input IMNMX)
+          // 4-score maxima, one vote for the whole 32-score row; then, per
+          // 4-score chunk some lane needs, a register-only append (rows stay
+          // in increasing order)
           int cm[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -267,25 +276,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
           const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                       max(cm[6], cm[7]));
           if (__any_sync(kFull, mx > thrd)) {
-            // slow path: stage the row in SMEM, then each lane walks only its
-            // passing 4-score chunks (rows stay in increasing order)
+            const uint32_t rb0 = (uint32_t)(lr0 + c0);
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              srow[i ^ (lane & 7)] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            unsigned cmask = 0;
+            for (int i = 0; i < 8; ++i) {
+              if (__any_sync(kFull, cm[i] > thrd)) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) cmask |= (cm[i] > thrd ? 1u : 0u) << i;
-            while (cmask) {
-              const int i = __ffs(cmask) - 1;
-              cmask &= cmask - 1;
-              const uint4 q4 = srow[i ^ (lane & 7)];
-              const int vv[4] = {(int)q4.x, (int)q4.y, (int)q4.z, (int)q4.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                if (vv[e] > thrd) my_buf[cnt++] = local_key(p.kf, vv[e], (uint32_t)(lr0 + c0 + 4 * i + e));
+                for (int j = 0; j < 4; ++j) {
+                  const int sc = (int)v[4 * i + j];
+                  if (sc > thrd) my_buf[cnt++] = local_key(p.kf, sc, rb0 + (uint32_t)(4 * i + j));
+                }
               }
             }
-            __syncwarp();
           }
         }
         tc_fence_before();
@@ -347,10 +348,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params p) {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+static int tc_bn(int NB) { return NB <= 8 ? tc::kBnWide : tc::kBnNarrow; }
+
 static int tc_stages(int NB) {
   const int a_bytes = tc::BM * NB * tc::KB;
-  const int budget = 227 * 1024 - a_bytes - tc::kEpiStageWords * 4 - 1024;
-  int s = budget / tc::kStageBytes;
+  const int stage_bytes = tc_bn(NB) * tc::KB;
+  const int budget = 227 * 1024 - a_bytes - 1024;
+  int s = budget / stage_bytes;
   if (s > 4) s = 4;
   return s;
 }
@@ -358,21 +362,23 @@ static int tc_stages(int NB) {
 // Work split: every SM gets one (query tile, DB chunk) item when the query
 // tiles do not cover the SMs: tile t gets s_lo or s_lo + 1 chunks so that the
 // item count equals the SM count.  Chunks are bounded by the local-key row
-// field (2^rb rows) and kept >= 4 tiles long.
+// field (2^rb rows) and kept >= 4 tiles long.  d <= 1024 runs N = 224 tiles,
+// 1024 < d <= 1536 N = 64 (the resident query tile takes 192 KB of SMEM).
 TcPlan plan_tc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   TcPlan pl{};
   const int NB = blocks128(d);
   pl.ok = false;
-  if (NB > 8 || nq < 1 || n < 1) return pl;
+  if (NB > 12 || nq < 1 || n < 1) return pl;
+  const int BN = tc_bn(NB);
   pl.stages = tc_stages(NB);
   if (pl.stages < 2) return pl;
   pl.ok = true;
   pl.n_qtiles = (int32_t)((nq + tc::BM - 1) / tc::BM);
-  pl.cap = k + 2 * tc::BN;
+  pl.cap = k + 2 * BN;
   const KeyFmt kf = make_keyfmt(d);
-  const int64_t lmax = ((int64_t)kf.rmask + 1) / tc::BN * tc::BN;
+  const int64_t lmax = ((int64_t)kf.rmask + 1) / BN * BN;
   const int64_t s_min = (n + lmax - 1) / lmax;                  // key-format bound
-  int64_t s_cap = (n + 4 * tc::BN - 1) / (4 * tc::BN);          // >= 4 tiles per chunk
+  int64_t s_cap = (n + 4 * BN - 1) / (4 * BN);                  // >= 4 tiles per chunk
   if (s_cap < s_min) s_cap = s_min;
   const int64_t QT = pl.n_qtiles;
   if (QT * s_min >= sms) {
@@ -387,19 +393,18 @@ TcPlan plan_tc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   pl.n_chunks = pl.s_lo + (pl.r_hi > 0 ? 1 : 0);
   pl.n_items = QT * pl.s_lo + pl.r_hi;
   pl.grid = (int32_t)(pl.n_items < sms ? pl.n_items : sms);
-  pl.smem = tc::BM * NB * tc::KB + pl.stages * tc::kStageBytes + tc::kEpiStageWords * 4 +
-            (2 * pl.stages + 4) * 8 + 16;
+  pl.smem = tc::BM * NB * tc::KB + pl.stages * BN * tc::KB + (2 * pl.stages + 4) * 8 + 16;
   pl.buf_bytes = (size_t)pl.grid * tc::BM * pl.cap * 4;
   pl.part_bytes = (size_t)pl.n_chunks * nq * k * 8;
   return pl;
 }
 
-template <int NB>
+template <int NB, int BN>
 static cudaError_t launch_tc_nb(const tc::Params& p, const TcPlan& pl, cudaStream_t st) {
-  auto kern = tc::scan_tc_kernel<NB>;
+  auto kern = tc::scan_tc_kernel<NB, BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<pl.grid, tc::kThreads, pl.smem, st>>>(p);
+  kern<<<pl.grid, tc::Cfg<BN>::kThreads, pl.smem, st>>>(p);
   note_launch();
   return cudaGetLastError();
 }
@@ -416,15 +421,20 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
   tc::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                (int32_t)pl.n_chunks, pl.n_items, pl.cap, pl.stages, bufs, part, thr0, thr0_stride,
                row_stride, dbg};
+  constexpr int W = tc::kBnWide, R = tc::kBnNarrow;
   switch (NB) {
-    case 1: return launch_tc_nb<1>(p, pl, st);
-    case 2: return launch_tc_nb<2>(p, pl, st);
-    case 3: return launch_tc_nb<3>(p, pl, st);
-    case 4: return launch_tc_nb<4>(p, pl, st);
-    case 5: return launch_tc_nb<5>(p, pl, st);
-    case 6: return launch_tc_nb<6>(p, pl, st);
-    case 7: return launch_tc_nb<7>(p, pl, st);
-    case 8: return launch_tc_nb<8>(p, pl, st);
+    case 1: return launch_tc_nb<1, W>(p, pl, st);
+    case 2: return launch_tc_nb<2, W>(p, pl, st);
+    case 3: return launch_tc_nb<3, W>(p, pl, st);
+    case 4: return launch_tc_nb<4, W>(p, pl, st);
+    case 5: return launch_tc_nb<5, W>(p, pl, st);
+    case 6: return launch_tc_nb<6, W>(p, pl, st);
+    case 7: return launch_tc_nb<7, W>(p, pl, st);
+    case 8: return launch_tc_nb<8, W>(p, pl, st);
+    case 9: return launch_tc_nb<9, R>(p, pl, st);
+    case 10: return launch_tc_nb<10, R>(p, pl, st);
+    case 11: return launch_tc_nb<11, R>(p, pl, st);
+    case 12: return launch_tc_nb<12, R>(p, pl, st);
     default: break;
   }
   return cudaErrorInvalidValue;

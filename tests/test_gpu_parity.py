@@ -175,9 +175,16 @@ def test_search_parity_shapes(uq, orc, algo, n, nq, k):
 
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("d,x", [(10, 5), (100, 67), (768, 384), (1000, 667), (1024, 256),
-                                 (1536, 768), (2048, 1024), (129, 1)])
+                                 (1152, 576), (1536, 768), (2048, 1024), (129, 1)])
 def test_search_parity_dims(uq, orc, algo, d, x):
     _search_case(uq, orc, algo, d, x, 6000, 150, 10, seed=d)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_search_parity_wide_d_seeded(uq, orc, algo):
+    """d = 1536 (config 4's width: the one-CTA tensor engine with N = 64 tiles),
+    several query tiles, a database large enough for threshold seeding."""
+    _search_case(uq, orc, algo, 1536, 768, 70001, 300, 100, seed=1536, mode="dup")
 
 
 @pytest.mark.parametrize("algo", ALGOS)
