@@ -30,8 +30,11 @@
 // one producer warp per sub-partition), warp 3 of the leader also issues the
 // MMAs, 4-11 epilogue in two sets of four (warp % 4 = TMEM lane quarter; set h
 // reads accumulator columns [128 h, 128 h + 128)).  12 warps = 3 per SM
-// sub-partition, whose 16K-register file allows 168 registers per thread (a
-// 13th warp would cap it at 128).
+// sub-partition, whose 16K-register file allows 168 registers per thread.
+// Measured alternatives: a dedicated 13th issuer warp caps registers at 128
+// and the producers slow down more than the issue gains (0.76 vs 0.65 ms on
+// c2); and TMEM epilogue warps must form whole aligned warpgroups (warps
+// 5..12 read the wrong lanes, 8..15 are correct).
 #include <cstdio>
 #include <cstdlib>
 
