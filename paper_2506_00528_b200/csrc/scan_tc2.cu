@@ -265,7 +265,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           for (int bb = 0; bb < kBlkPerStage; ++bb) {
             const int kb = ks * kBlkPerStage + bb;
             if (kb < NB) {
-              if (!(p.dbg & 1)) expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * 8) * B_LBO, B_LBO);
+              if (!(p.dbg & 1))
+                expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * 8) * B_LBO, B_LBO, !(p.dbg & 32));
               load_block(tile + 1, kb, dp[kb], dn[kb]);
             }
           }

@@ -152,7 +152,8 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 // One 128-dim block (uint4 of each plane) of one row -> 8 chunks of 16 B at
 // chunk addresses base + c * chunk_stride (c = 0..7).  Explicit st.shared
 // (a generic store would be translated per access).
-__device__ __forceinline__ void expand_block_store(uint4 p, uint4 n, uint8_t* base, uint32_t chunk_stride) {
+__device__ __forceinline__ void expand_block_store(uint4 p, uint4 n, uint8_t* base, uint32_t chunk_stride,
+                                                   bool store = true) {
   const uint32_t pw[4] = {p.x, p.y, p.z, p.w};
   const uint32_t nw[4] = {n.x, n.y, n.z, n.w};
   const uint32_t sbase = smem_u32(base);
@@ -160,8 +161,12 @@ __device__ __forceinline__ void expand_block_store(uint4 p, uint4 n, uint8_t* ba
   for (int w = 0; w < 4; ++w) {
     uint32_t o[8];
     expand_word(pw[w], nw[w], o);
-    st_shared_v4(sbase + (2 * w) * chunk_stride, o[0], o[1], o[2], o[3]);
-    st_shared_v4(sbase + (2 * w + 1) * chunk_stride, o[4], o[5], o[6], o[7]);
+    if (store) {
+      st_shared_v4(sbase + (2 * w) * chunk_stride, o[0], o[1], o[2], o[3]);
+      st_shared_v4(sbase + (2 * w + 1) * chunk_stride, o[4], o[5], o[6], o[7]);
+    } else {  // timing ablation: keep the ALU work, drop the SMEM traffic
+      asm volatile("" ::"r"(o[0] ^ o[1] ^ o[2] ^ o[3] ^ o[4] ^ o[5] ^ o[6] ^ o[7]));
+    }
   }
 }
 
