@@ -46,8 +46,11 @@ struct PopcParams {
   int64_t row_stride;   // DB row r of this scan is row r * row_stride of dbcodes
 };
 
-template <int NB>
-__global__ void __launch_bounds__(kScanThreads, (NB <= 10 ? 2 : 1)) scan_popc_kernel(PopcParams p) {
+// OCC: resident CTAs per SM the registers are capped for.  Few-query tiles
+// (the HBM-bound case, e.g. Q = 1) keep fewer values live and gain from a
+// third CTA's extra loads in flight; many-query tiles (POPC-bound) do not.
+template <int NB, int OCC>
+__global__ void __launch_bounds__(kScanThreads, OCC) scan_popc_kernel(PopcParams p) {
   extern __shared__ uint4 smem_u4[];
   uint4* s_qm = smem_u4;                              // [qt][NB]  q+ | q-
   uint4* s_qn = smem_u4 + (size_t)p.qt * NB;          // [qt][NB]  q-
@@ -151,13 +154,15 @@ __global__ void __launch_bounds__(kScanThreads, (NB <= 10 ? 2 : 1)) scan_popc_ke
 }
 
 // ---------------------------------------------------------------------------
+static int popc_occ(int NB, int qt) { return (NB <= 6 && qt <= 8) ? 3 : (NB <= 10 ? 2 : 1); }
+
 PopcPlan plan_popc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   PopcPlan pl{};
   const int NB = blocks128(d);
   pl.qt = (int32_t)(nq < 64 ? (nq > 0 ? nq : 1) : 64);
   pl.n_qtiles = (int32_t)((nq + pl.qt - 1) / pl.qt);
   pl.cap = k + 2 * kStageRows;
-  const int grid_max = sms * 2;
+  const int grid_max = sms * popc_occ(NB, pl.qt);   // resident CTAs (launch bounds)
   const KeyFmt kf = make_keyfmt(d);
   const int64_t lmax = ((int64_t)kf.rmask + 1) / kStageRows * kStageRows;
   int64_t s_des = (2 * (int64_t)grid_max + pl.n_qtiles - 1) / (pl.n_qtiles > 0 ? pl.n_qtiles : 1);
@@ -176,14 +181,21 @@ PopcPlan plan_popc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   return pl;
 }
 
-template <int NB>
-static cudaError_t launch_popc_nb(const PopcParams& p, const PopcPlan& pl, cudaStream_t st) {
-  auto kern = scan_popc_kernel<NB>;
+template <int NB, int OCC>
+static cudaError_t launch_popc_occ(const PopcParams& p, const PopcPlan& pl, cudaStream_t st) {
+  auto kern = scan_popc_kernel<NB, OCC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
   kern<<<pl.grid, kScanThreads, pl.smem, st>>>(p);
   note_launch();
   return cudaGetLastError();
+}
+
+template <int NB>
+static cudaError_t launch_popc_nb(const PopcParams& p, const PopcPlan& pl, cudaStream_t st) {
+  const int occ = popc_occ(NB, pl.qt);
+  if (NB <= 6 && occ == 3) return launch_popc_occ<NB, (NB <= 6 ? 3 : 2)>(p, pl, st);
+  return launch_popc_occ<NB, (NB <= 10 ? 2 : 1)>(p, pl, st);
 }
 
 cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
