@@ -386,6 +386,15 @@ def main():
         "gpu_launches": gpu_launches,
         "clocks": clk,
     }
+    if world == 1:
+        # recall@k of the ternary search vs exact fp32 cosine kNN on the
+        # pre-quantisation vectors (untimed; a sample of the step's queries)
+        from tools.recall import cosine_topk_fp32, recall_at_k
+        ns = min(nq, 100)
+        _, gt_i = cosine_topk_fp32(w, u_q[:ns], k, id_base=id_base, n=n_loc)
+        line["recall"] = {"k": k, "recall_at_k": recall_at_k(out[1][:ns], gt_i), "queries": ns,
+                          "ground_truth": "exact cosine, fp32 with TF32 off, on the float vectors "
+                                          "(pinned to the fp64 oracle within 1e-5 relative in tests/test_recall.py)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if rank == 0:
