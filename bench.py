@@ -152,12 +152,41 @@ def _oracle_sample(w, target_s: float):
     return n_s, nq_s, run, cores
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(w, target_s=10.0):
+    """The oracle as it stands, on the host's cores: all threads, then 1 thread
+    on a proportionally smaller query sample (BASELINE.md CPU plan)."""
+    import oracle
     n_s, nq_s, run, cores = _oracle_sample(w, target_s)
     t = run(nq_s)
+    prev = oracle.set_threads(1)
+    nq1 = max(1, nq_s // max(cores, 1))
+    t1 = run(nq1)
+    oracle.set_threads(prev)
     return {"value": nq_s * n_s / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1thread": nq1 * n_s / t1, "cpu_model": _cpu_model(),
             "sample": f"{nq_s} queries (oracle encode + exhaustive kNN, k={w.k}) over the first "
-                      f"{n_s} database rows of {w.name}; {t:.1f} s wall on {cores} host threads"}
+                      f"{n_s} database rows of {w.name}; {t:.1f} s wall on {cores} host threads "
+                      f"({nq1} queries, {t1:.1f} s on 1 thread)"}
+
+
+# The paper's own speed numbers for this path (context only, other hardware):
+PAPER_CONTEXT = {
+    "b2sp_per_delta": "21.8 ns per Delta (10^6 comparisons in 21.75 ms median), d=384, Apple M3, "
+                      "Rust BitVecSimd (P:463-476, Table 4): ~4.6e7 Delta-evals/s on one core",
+    "exhaustive_1M": "Table 5 (P:485-496), unstated hardware: d=768 Laion {512,768} b2sp 35.7 ms per "
+                     "~1M-row query (likelier reading: ~2.8e7 Delta-evals/s)",
+    "note": "no GPU numbers in the paper; BASELINE.md"}
 
 
 def run_reference(args, world, rank):
@@ -397,6 +426,7 @@ def main():
                                           "(pinned to the fp64 oracle within 1e-5 relative in tests/test_recall.py)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
+    line["paper_context"] = PAPER_CONTEXT
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

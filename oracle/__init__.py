@@ -61,6 +61,8 @@ def lib():
         L.orc_cosine_knn.argtypes = [vp, i64, vp, i64, i32, i32, vp, vp]
         L.orc_cosine_knn.restype = None
         L.orc_check_codes.argtypes = [vp, i64, i32]
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_threads.restype = ctypes.c_int
         L.orc_check_codes.restype = i64
         _lib = L
     return _lib
@@ -168,3 +170,8 @@ def cosine_knn(qv, dv, k: int):
 def check_codes(codes, d: int) -> int:
     c = np.ascontiguousarray(codes, dtype=np.uint8)
     return int(lib().orc_check_codes(_p(c), c.shape[0], d))
+
+
+def set_threads(n: int) -> int:
+    """Timing harness: worker threads of the oracle's OpenMP loops (returns the previous count)."""
+    return int(lib().orc_set_threads(n))

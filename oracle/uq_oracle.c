@@ -23,6 +23,9 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* Plane size of the packed code: 16 * ceil(d/128) bytes per plane (R6). */
 int64_t orc_plane_bytes(int32_t d) { return 16 * (((int64_t)d + 127) / 128); }
@@ -231,4 +234,18 @@ int64_t orc_check_codes(const uint8_t* codes, int64_t n, int32_t d) {
     bad += is_bad;
   }
   return bad;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Timing harness only (not arithmetic): worker threads of the OpenMP loops. */
+/* ------------------------------------------------------------------------ */
+int orc_set_threads(int n) {
+#ifdef _OPENMP
+  int prev = omp_get_max_threads();
+  if (n > 0) omp_set_num_threads(n);
+  return prev;
+#else
+  (void)n;
+  return 1;
+#endif
 }
