@@ -135,9 +135,9 @@ def _oracle_sample(w, target_s: float):
     """Time the oracle's encode(queries) + exhaustive kNN on a bounded sample of
     the workload: n_s database rows (oracle-encoded, untimed) x q_s queries."""
     import oracle
-    n_s = min(w.n, 20000)
+    n_s = min(w.n, 100_000)
     db = datagen.db(w, "cpu", 0, n_s).numpy()
-    q_all = datagen.rows(w, "q", 0, min(w.nq, 256), "cpu").numpy()
+    q_all = datagen.rows(w, "q", 0, min(w.nq, 1000), "cpu").numpy()
     o_db = oracle.pack(oracle.encode(db, w.x))
 
     def run(nq_s):
@@ -358,7 +358,9 @@ def main():
         achieved = ops / scan_avg_s / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": "scan_tc_kernel (int8 tcgen05 Delta GEMM + fused top-k)",
+                "kernel": ("scan_tc2_kernel (CTA-pair int8 tcgen05 Delta GEMM + fused top-k)"
+                           if nq > 128 and d <= 1024 else
+                           "scan_tc_kernel (int8 tcgen05 Delta GEMM + fused top-k)"),
                 "peak_source": f"2 x bf16_tflops of {peaks_src} MEASURED_PEAKS.json (int8 = 2x bf16 nominal)",
                 "algorithmic": "2*d ops per Delta (d int8 MACs)"}
     else:
