@@ -135,7 +135,7 @@ def _oracle_sample(w, target_s: float):
     """Time the oracle's encode(queries) + exhaustive kNN on a bounded sample of
     the workload: n_s database rows (oracle-encoded, untimed) x q_s queries."""
     import oracle
-    n_s = min(w.n, 100_000)
+    n_s = min(w.n, 200_000)
     db = datagen.db(w, "cpu", 0, n_s).numpy()
     q_all = datagen.rows(w, "q", 0, min(w.nq, 1000), "cpu").numpy()
     o_db = oracle.pack(oracle.encode(db, w.x))
@@ -146,9 +146,10 @@ def _oracle_sample(w, target_s: float):
         oracle.knn(o_q, o_db, w.d, w.k)
         return time.perf_counter() - t0
 
-    t1 = run(1)
     cores = os.cpu_count() or 1
-    nq_s = int(max(1, min(q_all.shape[0], target_s / max(t1, 1e-6) * min(cores, 8))))
+    ncal = min(q_all.shape[0], cores)          # one query per thread: a full-width calibration
+    tcal = run(ncal)
+    nq_s = int(max(1, min(q_all.shape[0], ncal * target_s / max(tcal, 1e-6))))
     return n_s, nq_s, run, cores
 
 
