@@ -1,5 +1,6 @@
 // api.cu -- the C ABI of libuq.so (declared and documented in include/uq.h):
 // synchronous argument validation, launch planning, workspace carving.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -115,9 +116,10 @@ static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
     return e ? atoi(e) : -1;
   }();
   int seed_div = div_env >= 0 ? div_env : (hist ? 8 : 32);
-  // large databases: ~512k sampled rows already bound D_k tightly for the
-  // configs' k (c5: 5e7 rows, k = 10); more only lengthens the seeding scan
-  if (div_env < 0 && n / seed_div > ((int64_t)1 << 19) && (int64_t)k <= 256) seed_div = (int)(n >> 19);
+  // large databases: max(2^17, 4096 k) sampled rows already bound D_k tightly
+  // (measured on c3 / c5: larger samples only lengthen the seeding scan)
+  const int64_t cap = std::max<int64_t>((int64_t)1 << 17, (int64_t)4096 * k);
+  if (div_env < 0 && n / seed_div > cap) seed_div = (int)std::min<int64_t>(n / cap, INT32_MAX);
   if (seed_div <= 0) return sp;
   if (n < (int64_t)1 << 16) return sp;
   int64_t rows = n / seed_div;
