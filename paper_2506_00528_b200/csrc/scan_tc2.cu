@@ -224,10 +224,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       const int r = threadIdx.x;
       const uint32_t full_dst = mapa(smem_u32(&full[0]), 0);  // leader's full[0]
       uint4 dp[NB], dn[NB];
+      // scan row -> database row: row_stride-strided rows (top-k mode), or in
+      // histogram mode whole BN-row blocks, one in every row_stride (the
+      // seeding sample stays spread over the database, and each block is
+      // contiguous for the L2 prefetch)
+      auto sample_row = [&](int64_t sr) -> int64_t {
+        if (MODE == kModeHist) return (sr / BN) * (BN * p.row_stride) + sr % BN;
+        return sr * p.row_stride;
+      };
       auto load_block = [&](int tile, int kb, uint4& a, uint4& b) {
         const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + r;
         if (tile < ntiles && lr < rows && !(p.dbg & 4)) {
-          const uint8_t* src = p.db + (row0 + lr) * p.row_stride * cb;
+          const uint8_t* src = p.db + sample_row(row0 + lr) * cb;
           a = __ldg(reinterpret_cast<const uint4*>(src) + kb);
           b = __ldg(reinterpret_cast<const uint4*>(src + pb) + kb);
         } else {
@@ -242,9 +250,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       // the register ring hides one tile of latency, L2 covers the rest
       auto prefetch_rows = [&](int tile) {
         const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + (r & ~31);
-        if (p.row_stride == 1 && lane == 0 && tile < ntiles && lr < rows) {
-          const int64_t nr = (rows - lr < 32) ? rows - lr : 32;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.db + (row0 + lr) * cb),
+        if ((MODE == kModeHist || p.row_stride == 1) && lane == 0 && tile < ntiles && lr < rows) {
+          const int64_t nr = (rows - lr < 32) ? rows - lr : 32;   // 32 rows stay inside one BN-row block
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.db + sample_row(row0 + lr) * cb),
                        "r"((uint32_t)(nr * cb)) : "memory");
         }
       };
