@@ -135,7 +135,9 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 }
 
 // 32 dims (one 32-bit word of each plane) -> 8 words of int8 in K-permuted order.
-// (Moving half the shifts to the FMA pipe as IMAD.HI measured slower.)
+// Measured alternatives (tools/expand_bench.cu, tc2_prof.py): half the shifts
+// as IMAD.HI on the FMA pipe, and (p_b + 255 n_b) >> b in 64 bits with one
+// shift for both planes, were both no faster than this form.
 __device__ __forceinline__ void expand_word(uint32_t p, uint32_t n, uint32_t (&o)[8]) {
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
