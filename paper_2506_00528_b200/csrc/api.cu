@@ -131,7 +131,7 @@ static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
 }
 
 struct SearchLayout {
-  size_t bufs_off, part_off, seed_s_off, seed_i_off, hist_off, total;
+  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, hist_off, total;
 };
 
 static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms,
@@ -147,7 +147,7 @@ static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t 
 }
 
 static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  SearchLayout L{0, 0, 0, 0, 0, 0};
+  SearchLayout L{0, 0, 0, 0, 0, 0, 0};
   if (nq == 0 || n == 0) return L;
   size_t bufs = 0, part = engine_bytes(a, nq, n, d, k, sms, &bufs);
   const bool hist = hist_seed(a, nq, d);
@@ -159,7 +159,10 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   }
   L.bufs_off = 0;
   L.part_off = bufs;
-  L.seed_s_off = L.part_off + part;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
+  L.cnt_off = L.part_off + part;      // [lists][nq] valid entries per list (pair engine)
+  const size_t cnt_bytes = (a == UQ_ALGO_TCGEN05 && use_pairs(nq, d))
+                               ? align_up((size_t)plan_tc2(nq, n, d, k, sms).n_chunks * nq * 4, 256) : 0;
+  L.seed_s_off = L.cnt_off + cnt_bytes;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
   L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * (hist ? 1 : k) * 4, 256) : 0);
   L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
   L.total = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 128 * 4, 256) : 0);
@@ -174,7 +177,7 @@ static size_t workspace_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t
 static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n,
                                   int32_t d, int32_t k, int64_t id_base, int64_t row_stride,
                                   const int32_t* thr0, int32_t thr0_stride, uint32_t* bufs,
-                                  uint64_t* part, int32_t* out_s, int64_t* out_id, int sms,
+                                  uint64_t* part, int32_t* part_cnt, int32_t* out_s, int64_t* out_id, int sms,
                                   int timer_kind, cudaStream_t st) {
   cudaEvent_t ev;
   int64_t lists = 0;
@@ -182,7 +185,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   timer_begin(st, &ev, timer_kind, (double)nq * (double)n);
   if (a == UQ_ALGO_TCGEN05) {
     const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
-    e = use_pairs(nq, d) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st)
+    e = use_pairs(nq, d) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, st)
                       : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
     lists = tp.n_chunks;
   } else {
@@ -192,7 +195,8 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   }
   timer_end(st, ev);
   if (e != cudaSuccess) return e;
-  return launch_merge_keys(part, lists, nq, k, k, id_base, out_s, out_id, st);
+  const bool counted = a == UQ_ALGO_TCGEN05 && use_pairs(nq, d);
+  return launch_merge_keys(part, lists, nq, k, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr);
 }
 
 }  // namespace uq
@@ -224,9 +228,9 @@ uq_status uq_timing_enable(int32_t on) {
 }
 
 // Debug (not in uq.h): CTA-pair scan cycle accounting under UQ_TC_ABLATE & 8.
-uq_status uq_debug_tc2_prof(unsigned long long* out16) {
-  if (!out16) return UQ_ERR_INVALID_ARG;
-  return from_cuda(tc2_prof_read(out16));
+uq_status uq_debug_tc2_prof(unsigned long long* out24) {
+  if (!out24) return UQ_ERR_INVALID_ARG;
+  return from_cuda(tc2_prof_read(out24));
 }
 
 uq_status uq_timing_collect_ex(double* scan_ms, int64_t* launches, double* delta_evals) {
@@ -329,6 +333,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   const SearchLayout L = layout_for(a, nq, n, d, k, sms);
   uint32_t* bufs = reinterpret_cast<uint32_t*>(ws + L.bufs_off);
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part_off);
+  int32_t* part_cnt = reinterpret_cast<int32_t*>(ws + L.cnt_off);
   const bool hist = hist_seed(a, nq, d);
   const SeedPlan sp = plan_seed(n, k, hist);
   const int32_t* thr0 = nullptr;
@@ -349,13 +354,13 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
     int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
     cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, sp.rows, d, k, 0, sp.stride, nullptr, 0,
-                                   bufs, part, seed_s, seed_i, sms, 1, st);
+                                   bufs, part, part_cnt, seed_s, seed_i, sms, 1, st);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = seed_s + (k - 1);  // k-th best sample Delta, row stride k
   }
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
   cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, thr0_stride, bufs, part,
-                                 out_scores, out_ids, sms, 0, st);
+                                 part_cnt, out_scores, out_ids, sms, 0, st);
   return from_cuda(e);
 }
 

@@ -21,7 +21,8 @@ cudaError_t launch_scores(const uint8_t* q, int64_t nq, const uint8_t* db, int64
 cudaError_t launch_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad,
                                int sms, cudaStream_t st);
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
-                              int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st);
+                              int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
+                              const int32_t* counts = nullptr);
 cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
                             int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st);
 
@@ -54,13 +55,13 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
 
 // Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128.
 TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
-cudaError_t tc2_prof_read(unsigned long long* out16);
+cudaError_t tc2_prof_read(unsigned long long* out24);
 TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms,
                                  cudaStream_t st);
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
-                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
+                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                             cudaStream_t st);
 

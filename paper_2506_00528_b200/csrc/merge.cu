@@ -32,6 +32,7 @@ struct MergeParams {
   int32_t* out_s;
   int64_t* out_id;
   int32_t stage_cap;  // candidates staged in shared memory if C <= stage_cap
+  const int32_t* counts;  // source (a), optional: valid entries per list [lists][nq] (rest unread, empty)
 };
 
 template <bool FROM_SI>
@@ -39,6 +40,7 @@ __device__ __forceinline__ uint64_t cand_key(const MergeParams& p, int64_t q, in
   const int64_t l = i / p.kin, e = i % p.kin;
   const size_t off = ((size_t)l * p.nq + q) * p.kin + e;
   if (FROM_SI) return global_key(p.scores[off], p.ids[off]);
+  if (p.counts != nullptr && e >= p.counts[(size_t)l * p.nq + q]) return 0ull;
   return p.keys[off];
 }
 
@@ -184,14 +186,15 @@ static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t
 }
 
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
-                              int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
-  MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0};
+                              int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
+                              const int32_t* counts) {
+  MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0, counts};
   return launch_merge_common(p, false, st);
 }
 
 cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
                             int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
-  MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0};
+  MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0, nullptr};
   return launch_merge_common(p, true, st);
 }
 

@@ -80,6 +80,7 @@ struct Params {
   int32_t stages;
   uint32_t* bufs;       // [gridDim.x][kEpiSets*BM][cap]
   uint64_t* part;       // [s_max*kEpiSets][nq][k]
+  int32_t* part_cnt;    // [s_max*kEpiSets][nq] valid entries of each list
   const int32_t* thr0;  // optional per-query seed D_k (rows with Delta < D_k cannot matter)
   int32_t thr0_stride;
   int64_t row_stride;
@@ -93,8 +94,10 @@ struct Params {
 // Cycle accounting (ablation/profiling only: dbg & 8), read by uq_tc2_prof:
 // 0 MMA item loop, 1 MMA wait tempty, 2 MMA wait full, 3 producer loop, 4
 // producer wait empty, 5 epilogue loop, 6 epilogue wait tfull, 7 epilogue
-// TMEM load + filter, 8 epilogue rebuilds, 9 epilogue publish, 10 items.
-__device__ unsigned long long g_prof[16];
+// TMEM load + filter, 8 epilogue rebuilds, 9 epilogue publish, 10 items,
+// 11 CTA setup, 12 CTA item loop, 13 CTA teardown, 14 CTAs (thread 0 of each),
+// 15 appended candidates, 16 in-loop stream cuts, 17 streams cut at the end.
+__device__ unsigned long long g_prof[24];
 __device__ __forceinline__ long long clk() { return clock64(); }
 #define PROF_ON (MODE == kModeTopK && (p.dbg & 8))
 #define PROF_ADD(i, v) do { if (PROF_ON && lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(v)); } while (0)
@@ -159,6 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t_entry = PROF_ON ? clk() : 0;
   const uint32_t cr = cluster_ctarank();
   const bool leader = cr == 0;
   const int64_t pb = (int64_t)NB * 16, cb = 2 * pb;
@@ -183,6 +187,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
+  const long long t_setup = PROF_ON ? clk() : 0;
+  if (threadIdx.x == 0) PROF_ADD(11, t_setup - t_entry);
 
   int stage = 0;            // producers: next stage to fill
   uint32_t sphase = 0;
@@ -407,6 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
         uint32_t* const wbufs = p.bufs + ((size_t)blockIdx.x * kEpiSets * BM + sidx) * p.cap;
         uint32_t* const my_buf = wbufs + (size_t)lane * p.cap;
         int cnt = 0;
+        unsigned n_app = 0, n_reb = 0;   // cycle accounting only: appended keys, in-loop cuts
         int thrd = INT32_MIN;  // a score passes iff Delta > thrd
         if (p.thr0 && qme < p.nq) {
           const int32_t dk = p.thr0[qme * p.thr0_stride];
@@ -448,7 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const int sc = (int)v[4 * i + j];
-                    if (sc > thrd) my_buf[cnt++] = local_key(p.kf, sc, rb0 + (uint32_t)(4 * i + j));
+                    if (sc > thrd) { my_buf[cnt++] = local_key(p.kf, sc, rb0 + (uint32_t)(4 * i + j)); ++n_app; }
                   }
                 }
               }
@@ -469,11 +476,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
             if (lane == L) {
               cnt = p.k;
               thrd = max(thrd, (int)D - p.kf.off);
+              ++n_reb;
             }
           }
           if (PROF_ON) t_r += clk() - t2;
         }
         long long t_pub = PROF_ON ? clk() : 0;
+        if (PROF_ON) {
+          const unsigned a = __reduce_add_sync(kFull, n_app), rb = __reduce_add_sync(kFull, n_reb);
+          const unsigned fin = __popc(__ballot_sync(kFull, cnt > p.k));
+          PROF_ADD(15, a);
+          PROF_ADD(16, rb);
+          PROF_ADD(17, fin);
+        }
         PROF_ADD(5, t_pub - t_loop);
         PROF_ADD(6, t_w);
         PROF_ADD(7, t_f);
@@ -489,30 +504,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           if (lane == L) cnt = p.k;
         }
         __syncwarp();
-        for (int L = 0; L < 32; ++L) {
-          const int64_t qi = q0 + quarter * 32 + L;
-          const int cL = __shfl_sync(kFull, cnt, L);
-          if (qi >= p.nq) continue;
-          const uint32_t* bL = wbufs + (size_t)L * p.cap;
-          uint64_t* out = p.part + ((size_t)(it.c * kEpiSets + h) * p.nq + qi) * p.k;
-          for (int i = lane; i < p.k; i += 32)
-            out[i] = (i < cL) ? global_key_from_local(p.kf, bL[i], (uint64_t)row0) : 0ull;
-          if (it.c == it.s_t - 1)
-            for (int c2 = it.s_t; c2 < p.s_max; ++c2) {
-              uint64_t* z = p.part + ((size_t)(c2 * kEpiSets + h) * p.nq + qi) * p.k;
-              for (int i = lane; i < p.k; i += 32) z[i] = 0ull;
+        // publish: 8 streams x 4 entries per lane per round, all loads issued
+        // before the stores (a stream-at-a-time loop serialised ~100 L2 round
+        // trips per warp: 25 us of every work item's tail on c2)
+        for (int L0 = 0; L0 < 32; L0 += 8) {
+          for (int i0 = 0; i0 < p.k; i0 += 128) {
+            uint32_t t[8][4];
+            int cLs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              cLs[u] = __shfl_sync(kFull, cnt, L0 + u);
+              const uint32_t* bL = wbufs + (size_t)(L0 + u) * p.cap;
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const int i = i0 + 32 * v + lane;
+                t[u][v] = (i < cLs[u] && i < p.k) ? bL[i] : 0u;
+              }
             }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int64_t qi = q0 + quarter * 32 + L0 + u;
+              if (qi >= p.nq) continue;
+              const size_t list = (size_t)(it.c * kEpiSets + h) * p.nq + qi;
+              uint64_t* out = p.part + list * p.k;
+              const int cv = min(cLs[u], p.k);
+              if (i0 == 0 && lane == 0) p.part_cnt[list] = cv;   // entries past it are never read
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const int i = i0 + 32 * v + lane;
+                if (i < cv) out[i] = global_key_from_local(p.kf, t[u][v], (uint64_t)row0);
+              }
+            }
+          }
+        }
+        if (it.c == it.s_t - 1) {   // tiles with fewer chunks than s_max: the unused lists are empty
+          const int64_t qi = q0 + quarter * 32 + lane;
+          if (qi < p.nq)
+            for (int c2 = it.s_t; c2 < p.s_max; ++c2) p.part_cnt[(size_t)(c2 * kEpiSets + h) * p.nq + qi] = 0;
         }
         PROF_ADD(9, clk() - t_pub);
       }
     }
   }
+  const long long t_items = PROF_ON ? clk() : 0;
+  if (threadIdx.x == 0) PROF_ADD(12, t_items - t_setup);
   tc_fence_before();
   cluster_sync();
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc2(tmem_base, kTmemCols);
   }
+  if (threadIdx.x == 0) PROF_ADD(13, clk() - t_items);
+  if (threadIdx.x == 0) PROF_ADD(14, 1);
 }
 
 // kHist -> per-query seed: thr[q] = (largest b with sum_{b' >= b} hist[q][b'] >= k) << hshift,
@@ -650,20 +693,20 @@ static int tc2_dbg() {
 }
 
 // profiling counters (dbg & 8): copy out and reset
-cudaError_t tc2_prof_read(unsigned long long* out16) {
-  cudaError_t e = cudaMemcpyFromSymbol(out16, tc2::g_prof, 16 * sizeof(unsigned long long));
+cudaError_t tc2_prof_read(unsigned long long* out24) {
+  cudaError_t e = cudaMemcpyFromSymbol(out24, tc2::g_prof, 24 * sizeof(unsigned long long));
   if (e != cudaSuccess) return e;
-  static const unsigned long long z[16] = {0};
+  static const unsigned long long z[24] = {0};
   return cudaMemcpyToSymbol(tc2::g_prof, z, sizeof(z));
 }
 
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
-                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part,
+                            int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                             cudaStream_t st) {
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
-                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, bufs, part, thr0, thr0_stride,
-                row_stride, nullptr, 0, 0.f, tc2_dbg()};
+                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
+                thr0_stride, row_stride, nullptr, 0, 0.f, tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), st);
 }
 
@@ -682,8 +725,8 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   float z = inv_norm_cdf(1.0 - ptail);
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
-                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr, 0,
-                row_stride, ghist, hs, z, tc2_dbg()};
+                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
+                nullptr, 0, row_stride, ghist, hs, z, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, k, hs, thr);

@@ -22,7 +22,7 @@ q = uq.encode(datagen.queries(w, "cuda"), w.x)
 ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, uq.ALGO_TCGEN05), dtype=torch.uint8, device="cuda")
 L = uq._L
 L.uq_debug_tc2_prof.argtypes = [ctypes.c_void_p]
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 24)()
 for _ in range(2):
     uq.search(q, db, w.d, w.k, algo=uq.ALGO_TCGEN05, workspace=ws)
 torch.cuda.synchronize()
@@ -38,5 +38,9 @@ out = {"cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
        "prod_wait_empty_frac": c[4] / max(c[3], 1),
        "epi_wait_tfull_frac": c[6] / max(c[5], 1), "epi_filter_frac": c[7] / max(c[5], 1),
        "epi_rebuild_frac": c[8] / max(c[5], 1), "epi_publish_over_loop": c[9] / max(c[5], 1),
-       "mma_loop_cycles_per_item": c[0] / max(c[10], 1), "raw": c}
+       "mma_loop_cycles_per_item": c[0] / max(c[10], 1),
+       "cta_setup_cycles": c[11] / max(c[14], 1), "cta_items_cycles": c[12] / max(c[14], 1),
+       "cta_teardown_cycles": c[13] / max(c[14], 1),
+       "candidates_per_query": c[15] / max(w.nq * reps, 1), "inloop_cuts_per_query": c[16] / max(w.nq * reps, 1),
+       "final_cuts_per_query": c[17] / max(w.nq * reps, 1), "raw": c}
 print(json.dumps(out))
