@@ -301,12 +301,16 @@ def main():
     _barrier(world)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     t0.record()
-    for _ in range(args.steps):
+    marks[0].record()
+    for st in range(args.steps):
         step(u_q)
+        marks[st + 1].record()
     t1.record()
     torch.cuda.synchronize()
     _barrier(world)
+    step_ms = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
     uq.timing_enable(False)
     clk = clocks.stop()
     gpu_launches = launches[0]
@@ -344,6 +348,11 @@ def main():
     evals_per_step = nq * n_loc * world
     value = evals_per_step * args.steps / (ms * 1e-3)
     e2e_value = evals_per_step * args.steps / (e2e_ms * 1e-3)
+
+    # the timed run's result equals an untimed run's, byte for byte
+    s_timed, i_timed = out[0].clone(), out[1].clone()
+    s_chk, i_chk = step(u_q)
+    checksum_ok = bool(torch.equal(s_chk, s_timed) and torch.equal(i_chk, i_timed))
 
     peaks, peaks_src = _peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
@@ -416,6 +425,8 @@ def main():
                 "h2d_bytes_per_step": u_q.numel() * u_q.element_size(),
                 "d2h_bytes_per_step": nq * k * (4 + 8)},
         "gpu_launches": gpu_launches,
+        "step_ms": {"median": statistics.median(step_ms), "min": step_ms[0], "max": step_ms[-1]},
+        "checksum_equal_untimed_run": checksum_ok,
         "clocks": clk,
     }
     if world == 1:
