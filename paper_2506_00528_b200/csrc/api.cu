@@ -195,8 +195,10 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   }
   timer_end(st, ev);
   if (e != cudaSuccess) return e;
+  // the pair engine publishes variable-length lists of up to cap entries with counts
   const bool counted = a == UQ_ALGO_TCGEN05 && use_pairs(nq, d);
-  return launch_merge_keys(part, lists, nq, k, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr);
+  const int32_t kin = counted ? plan_tc2(nq, n, d, k, sms).cap : k;
+  return launch_merge_keys(part, lists, nq, kin, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr);
 }
 
 }  // namespace uq

@@ -18,6 +18,7 @@ namespace uq {
 
 constexpr int kMergeThreads = 256;
 constexpr int kMergeWarps = kMergeThreads / 32;
+constexpr int kMergeMaxLists = 1024;   // counted lists gathered compactly up to this many
 
 struct MergeParams {
   // source (a): keys [lists][nq][k]; source (b): scores/ids [lists][nq][k]
@@ -57,17 +58,51 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   __shared__ int s_b, s_above, s_inb;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = blockIdx.x;
-  const int64_t C = p.lists * p.kin;
+  __shared__ int s_off[kMergeMaxLists + 1];
+  int64_t C = p.lists * p.kin;
   const int P = 1 << bitlen((unsigned)(p.k - 1 > 0 ? p.k - 1 : 1));  // pow2 >= k (>= 2)
   uint64_t* s_sel = smem_u64;          // [P]
   uint64_t* s_cand = smem_u64 + P;     // [stage_cap] (if staged)
-  const bool staged = C <= p.stage_cap;
+  bool staged = C <= p.stage_cap;
+  bool compact = false;
+  // counted lists: gather only the valid entries, contiguously, into SMEM
+  if (!FROM_SI && p.counts != nullptr && p.lists <= kMergeMaxLists) {
+    if (warp == 0) {
+      int base = 0;
+      for (int64_t l0 = 0; l0 < p.lists; l0 += 32) {
+        const int64_t l = l0 + lane;
+        const int c = (l < p.lists) ? min(p.counts[(size_t)l * p.nq + q], p.kin) : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += t;
+        }
+        if (l < p.lists) s_off[l] = base + incl - c;
+        base += __shfl_sync(kFull, incl, 31);
+      }
+      if (lane == 0) s_off[p.lists] = base;
+    }
+    __syncthreads();
+    const int total = s_off[p.lists];
+    if (total <= p.stage_cap) {
+      for (int64_t l = warp; l < p.lists; l += kMergeWarps) {
+        const int o = s_off[l], c = s_off[l + 1] - o;
+        const uint64_t* src = p.keys + ((size_t)l * p.nq + q) * p.kin;
+        for (int e = lane; e < c; e += 32) s_cand[o + e] = src[e];
+      }
+      C = total;
+      staged = true;
+      compact = true;
+      __syncthreads();
+    }
+  }
   // stage + common bits of the valid (non-zero) keys
   uint64_t a_and = ~0ull, a_or = 0ull;
   unsigned nv = 0;
   for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) {
-    const uint64_t key = cand_key<FROM_SI>(p, q, i);
-    if (staged) s_cand[i] = key;
+    const uint64_t key = compact ? s_cand[i] : cand_key<FROM_SI>(p, q, i);
+    if (staged && !compact) s_cand[i] = key;
     if (key != 0ull) { a_and &= key; a_or |= key; ++nv; }
   }
   a_and = __reduce_and_sync(kFull, (unsigned)a_and) | ((uint64_t)__reduce_and_sync(kFull, (unsigned)(a_and >> 32)) << 32);
@@ -164,8 +199,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
 
 static int merge_smem(int32_t k, int64_t C, int32_t* stage_cap) {
   const int P = 1 << bitlen((unsigned)(k - 1 > 0 ? k - 1 : 1));
-  const int64_t budget = 96 * 1024 / 8 - P;  // keys that fit beside s_sel
-  *stage_cap = (int32_t)(C <= budget ? C : 0);
+  const int64_t budget = 48 * 1024 / 8 - P;  // keys staged beside s_sel (4 CTAs per SM)
+  *stage_cap = (int32_t)(C <= budget ? C : budget);   // lists larger than this are read from global
   return (int)((P + *stage_cap) * 8);
 }
 

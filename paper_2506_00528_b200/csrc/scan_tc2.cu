@@ -79,7 +79,7 @@ struct Params {
   int32_t cap;
   int32_t stages;
   uint32_t* bufs;       // [gridDim.x][kEpiSets*BM][cap]
-  uint64_t* part;       // [s_max*kEpiSets][nq][k]
+  uint64_t* part;       // [s_max*kEpiSets][nq][cap] (top-k mode)
   int32_t* part_cnt;    // [s_max*kEpiSets][nq] valid entries of each list
   const int32_t* thr0;  // optional per-query seed D_k (rows with Delta < D_k cannot matter)
   int32_t thr0_stride;
@@ -493,22 +493,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
         PROF_ADD(6, t_w);
         PROF_ADD(7, t_f);
         PROF_ADD(8, t_r);
-        // finalize: cut to k, publish global keys as list (chunk, set)
-        __syncwarp();
-        unsigned need = __ballot_sync(kFull, cnt > p.k);
-        while (need) {
-          const int L = __ffs(need) - 1;
-          need &= need - 1;
-          const int cL = __shfl_sync(kFull, cnt, L);
-          ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
-          if (lane == L) cnt = p.k;
-        }
+        // finalize: publish each stream's candidates as list (chunk, set), all
+        // cnt <= cap of them -- a superset of the stream's top-k, so the merge
+        // stays exact, without the warp-serial cut of every stream to k (with
+        // k = 10 nearly every stream needed one: 85 us of c5's kernel tail)
         __syncwarp();
         // publish: 8 streams x 4 entries per lane per round, all loads issued
         // before the stores (a stream-at-a-time loop serialised ~100 L2 round
         // trips per warp: 25 us of every work item's tail on c2)
         for (int L0 = 0; L0 < 32; L0 += 8) {
-          for (int i0 = 0; i0 < p.k; i0 += 128) {
+          for (int i0 = 0; i0 < p.cap; i0 += 128) {
             uint32_t t[8][4];
             int cLs[8];
 #pragma unroll
@@ -518,7 +512,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
                 const int i = i0 + 32 * v + lane;
-                t[u][v] = (i < cLs[u] && i < p.k) ? bL[i] : 0u;
+                t[u][v] = (i < cLs[u]) ? bL[i] : 0u;
               }
             }
 #pragma unroll
@@ -526,8 +520,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
               const int64_t qi = q0 + quarter * 32 + L0 + u;
               if (qi >= p.nq) continue;
               const size_t list = (size_t)(it.c * kEpiSets + h) * p.nq + qi;
-              uint64_t* out = p.part + list * p.k;
-              const int cv = min(cLs[u], p.k);
+              uint64_t* out = p.part + list * p.cap;
+              const int cv = cLs[u];
               if (i0 == 0 && lane == 0) p.part_cnt[list] = cv;   // entries past it are never read
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
@@ -643,7 +637,7 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   pl.smem = 1024 + tc2::BM * NB * tc2::KB + pl.stages * tc2::kStageBytes +
             (mode == tc2::kModeHist ? tc2::kHistBytes : 0) + (2 * pl.stages + 4) * 8 + 16;
   pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * tc2::kEpiSets * tc2::BM * pl.cap * 4;
-  pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * k * 8;
+  pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * pl.cap * 8;
   return pl;
 }
 

@@ -180,6 +180,12 @@ def test_search_parity_dims(uq, orc, algo, d, x):
     _search_case(uq, orc, algo, d, x, 6000, 150, 10, seed=d)
 
 
+def test_search_parity_large_k_pairs(uq, orc):
+    """Pair engine with k = 1000: counted candidate lists larger than the merge's
+    shared-memory stage (its global-memory fallback) and many in-loop cuts."""
+    _search_case(uq, orc, "tc", 384, 192, 300_000, 200, 1000, seed=77, mode="dup")
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 def test_search_parity_wide_d_seeded(uq, orc, algo):
     """d = 1536 (config 4's width: the one-CTA tensor engine with N = 64 tiles),
