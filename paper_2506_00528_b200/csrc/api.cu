@@ -230,9 +230,9 @@ uq_status uq_timing_enable(int32_t on) {
 }
 
 // Debug (not in uq.h): CTA-pair scan cycle accounting under UQ_TC_ABLATE & 8.
-uq_status uq_debug_tc2_prof(unsigned long long* out24) {
-  if (!out24) return UQ_ERR_INVALID_ARG;
-  return from_cuda(tc2_prof_read(out24));
+uq_status uq_debug_tc2_prof(unsigned long long* out48) {
+  if (!out48) return UQ_ERR_INVALID_ARG;
+  return from_cuda(tc2_prof_read(out48));
 }
 
 uq_status uq_timing_collect_ex(double* scan_ms, int64_t* launches, double* delta_evals) {

@@ -55,7 +55,7 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
 
 // Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128.
 TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
-cudaError_t tc2_prof_read(unsigned long long* out24);
+cudaError_t tc2_prof_read(unsigned long long* out48);
 TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms,

@@ -97,10 +97,10 @@ struct Params {
 // TMEM load + filter, 8 epilogue rebuilds, 9 epilogue publish, 10 items,
 // 11 CTA setup, 12 CTA item loop, 13 CTA teardown, 14 CTAs (thread 0 of each),
 // 15 appended candidates, 16 in-loop stream cuts, 17 streams cut at the end.
-__device__ unsigned long long g_prof[24];
+__device__ unsigned long long g_prof[48];   // [0, 24): top-k mode, [24, 48): histogram mode
 __device__ __forceinline__ long long clk() { return clock64(); }
-#define PROF_ON (MODE == kModeTopK && (p.dbg & 8))
-#define PROF_ADD(i, v) do { if (PROF_ON && lane == 0) atomicAdd(&g_prof[i], (unsigned long long)(v)); } while (0)
+#define PROF_ON ((p.dbg & 8) != 0)
+#define PROF_ADD(i, v) do { if (PROF_ON && lane == 0) atomicAdd(&g_prof[(i) + (MODE == kModeHist ? 24 : 0)], (unsigned long long)(v)); } while (0)
 
 struct Item {
   int t, c, s_t;
@@ -135,7 +135,7 @@ __device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* 
   for (int w = 0; w < kHistBins / 2; ++w) {
     uint32_t* cell = s_hist + w * BM + col;
     const uint32_t v = atomicExch(cell, 0u);
-    if (g != nullptr) {
+    if (g != nullptr) {   // (timing ablation UQ_TC_ABLATE & 64 passes g = nullptr)
       if (v & 0xffffu) atomicAdd(g + 2 * w, v & 0xffffu);
       if (v >> 16) atomicAdd(g + 2 * w + 1, v >> 16);
     }
@@ -406,8 +406,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           }
         }
         named_bar_sync(1 + quarter, 64);
-        if (h == 0) hist_flush(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBins : nullptr);
+        const long long tf0 = (p.dbg & 8) ? clk() : 0;
+        if (h == 0) hist_flush(s_hist, col, (qme < p.nq && !(p.dbg & 64)) ? p.ghist + (size_t)qme * kHistBins : nullptr);
         named_bar_sync(1 + quarter, 64);
+        if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[18], (unsigned long long)(clk() - tf0));
+        if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[19], 1ull);
       } else {
         const int sidx = h * BM + quarter * 32; // first stream of this warp
         uint32_t* const wbufs = p.bufs + ((size_t)blockIdx.x * kEpiSets * BM + sidx) * p.cap;
@@ -687,10 +690,10 @@ static int tc2_dbg() {
 }
 
 // profiling counters (dbg & 8): copy out and reset
-cudaError_t tc2_prof_read(unsigned long long* out24) {
-  cudaError_t e = cudaMemcpyFromSymbol(out24, tc2::g_prof, 24 * sizeof(unsigned long long));
+cudaError_t tc2_prof_read(unsigned long long* out48) {
+  cudaError_t e = cudaMemcpyFromSymbol(out48, tc2::g_prof, 48 * sizeof(unsigned long long));
   if (e != cudaSuccess) return e;
-  static const unsigned long long z[24] = {0};
+  static const unsigned long long z[48] = {0};
   return cudaMemcpyToSymbol(tc2::g_prof, z, sizeof(z));
 }
 

@@ -22,7 +22,7 @@ q = uq.encode(datagen.queries(w, "cuda"), w.x)
 ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, uq.ALGO_TCGEN05), dtype=torch.uint8, device="cuda")
 L = uq._L
 L.uq_debug_tc2_prof.argtypes = [ctypes.c_void_p]
-buf = (ctypes.c_ulonglong * 24)()
+buf = (ctypes.c_ulonglong * 48)()
 for _ in range(2):
     uq.search(q, db, w.d, w.k, algo=uq.ALGO_TCGEN05, workspace=ws)
 torch.cuda.synchronize()
@@ -42,5 +42,10 @@ out = {"cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
        "cta_setup_cycles": c[11] / max(c[14], 1), "cta_items_cycles": c[12] / max(c[14], 1),
        "cta_teardown_cycles": c[13] / max(c[14], 1),
        "candidates_per_query": c[15] / max(w.nq * reps, 1), "inloop_cuts_per_query": c[16] / max(w.nq * reps, 1),
-       "final_cuts_per_query": c[17] / max(w.nq * reps, 1), "raw": c}
+       "final_cuts_per_query": c[17] / max(w.nq * reps, 1),
+       "hist": {"mma_loop_cycles_per_item": c[24] / max(c[34], 1), "mma_wait_tempty_frac": c[25] / max(c[24], 1),
+                "mma_wait_full_frac": c[26] / max(c[24], 1), "prod_wait_empty_frac": c[28] / max(c[27], 1),
+                "cta_setup_cycles": c[35] / max(c[38], 1), "cta_items_cycles": c[36] / max(c[38], 1),
+                "cta_teardown_cycles": c[37] / max(c[38], 1), "items": c[34]},
+       "raw": c}
 print(json.dumps(out))
