@@ -146,6 +146,27 @@ uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d,
                          unsigned long long* bad_rows, uq_stream_t stream);
 
 /*
+ * uq_rerank -- k@n: re-rank proxy-space candidates in the original space
+ * (Sec. 5.3: "n > k results are found from the approximate search,
+ * which are then reordered with respect to the original space, with the best k
+ * then selected").  For query i the candidates cand[i][0..n_cand) (database
+ * row ids, e.g. uq_search's ids with k = n_cand; ids < 0 or >= n are skipped;
+ * ids must be distinct) are scored by cosine similarity of the float vectors and the
+ * best k kept, ordered by (cos desc, id asc).
+ *   q       [nq][ldq] query vectors, element type dt (f32 / f16 / bf16)
+ *   db      [n][ld] database vectors, same dt (the vectors the codes came from)
+ *   cand    [nq][n_cand] int64, 1 <= n_cand <= UQ_MAX_K
+ *   out_cos [nq][k] f32 cosines (fp32 arithmetic; padding -inf), out_ids
+ *           [nq][k] int64 (padding -1), 1 <= k <= n_cand.
+ * Errors: UQ_ERR_INVALID_ARG for bad sizes / null pointers / misaligned
+ * vectors, UQ_ERR_UNSUPPORTED for d > UQ_MAX_D, n_cand > UQ_MAX_K or
+ * n >= 2^32 - 1.  Fewer than k valid candidates pad the tail.
+ */
+uq_status uq_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, const void* db, int64_t n,
+                    int64_t ld, int32_t d, const int64_t* cand, int32_t n_cand, int32_t k,
+                    float* out_cos, int64_t* out_ids, uq_stream_t stream);
+
+/*
  * Device-side timing of the scan kernels (the dominant kernel of uq_search), for
  * roofline accounting.  While enabled on a host thread, each scan launch issued
  * from that thread is bracketed by CUDA events on its stream.  collect() waits

@@ -62,6 +62,8 @@ def lib():
         L.orc_cosine_knn.restype = None
         L.orc_check_codes.argtypes = [vp, i64, i32]
         L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_rerank.argtypes = [vp, i64, vp, i64, i32, vp, i32, i32, vp, vp]
+        L.orc_rerank.restype = None
         L.orc_set_threads.restype = ctypes.c_int
         L.orc_check_codes.restype = i64
         _lib = L
@@ -164,6 +166,19 @@ def cosine_knn(qv, dv, k: int):
     s = np.zeros((nq, k), dtype=np.float64)
     ids = np.zeros((nq, k), dtype=np.int64)
     lib().orc_cosine_knn(_p(q), nq, _p(db), n, d, k, _p(s), _p(ids))
+    return s, ids
+
+
+def rerank(qv, dv, cand, k: int):
+    """k@n re-rank in fp64: cosine of each candidate id, (cos desc, id asc),
+    top k: (cos[nq][k] f64, ids[nq][k] int64)."""
+    q = _as_f64_rows(qv)
+    db = _as_f64_rows(dv)
+    c = np.ascontiguousarray(cand, dtype=np.int64)
+    nq, d = q.shape
+    s = np.zeros((nq, k), dtype=np.float64)
+    ids = np.zeros((nq, k), dtype=np.int64)
+    lib().orc_rerank(_p(q), nq, _p(db), db.shape[0], d, _p(c), c.shape[1], k, _p(s), _p(ids))
     return s, ids
 
 

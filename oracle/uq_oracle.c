@@ -217,6 +217,39 @@ void orc_cosine_knn(const double* qv, int64_t nq, const double* dv, int64_t n, i
   }
 }
 
+/* ------------------------------------------------------------------------ */
+/* k@n re-rank (Sec. 5.3): the candidates of the approximate       */
+/* search are "reordered with respect to the original space, with the best k */
+/* then selected" -- fp64 cosine of each candidate, (cos desc, id asc), top k. */
+/* ------------------------------------------------------------------------ */
+void orc_rerank(const double* qv, int64_t nq, const double* dv, int64_t n, int32_t d,
+                const int64_t* cand, int32_t n_cand, int32_t k, double* out_s, int64_t* out_id) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < nq; ++q) {
+    orc_fcand_t* c = (orc_fcand_t*)malloc(sizeof(orc_fcand_t) * (size_t)n_cand);
+    const double* a = qv + q * d;
+    const double na = norm2(a, d);
+    int32_t m = 0;
+    for (int32_t j = 0; j < n_cand; ++j) {
+      const int64_t id = cand[q * n_cand + j];
+      if (id < 0 || id >= n) continue;
+      const double* b = dv + id * d;
+      const double nb = norm2(b, d);
+      double dot = 0.0;
+      for (int32_t i = 0; i < d; ++i) dot += (a[i] / na) * (b[i] / nb);
+      c[m].s = dot;
+      c[m].id = id;
+      ++m;
+    }
+    qsort(c, (size_t)m, sizeof(orc_fcand_t), cmp_fcand);
+    for (int32_t j = 0; j < k; ++j) {
+      out_s[q * k + j] = (j < m) ? c[j].s : -INFINITY;
+      out_id[q * k + j] = (j < m) ? c[j].id : -1;
+    }
+    free(c);
+  }
+}
+
 /* Rows whose code is not a valid packed ternary vector: a position set in both
  * planes (pos AND neg != 0, the invariant of P:369-372), or a set pad bit (R6). */
 int64_t orc_check_codes(const uint8_t* codes, int64_t n, int32_t d) {

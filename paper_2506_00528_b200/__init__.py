@@ -17,7 +17,7 @@ import torch
 __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
     "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05",
-    "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex",
+    "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex", "rerank",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -50,6 +50,7 @@ def _load():
     L.uq_search_workspace_ex.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(sz)]
     L.uq_search_ex.argtypes = [vp, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, i32, vp]
     L.uq_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
+    L.uq_rerank.argtypes = [vp, i32, i64, i64, vp, i64, i64, i32, vp, i32, i32, vp, vp, vp]
     L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
     L.uq_timing_enable.argtypes = [i32]
@@ -57,7 +58,7 @@ def _load():
     L.uq_timing_collect_ex.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
                                        ctypes.POINTER(ctypes.c_double)]
     for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_timing_collect_ex", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
-              "uq_check_codes"):
+              "uq_check_codes", "uq_rerank"):
         getattr(L, f).restype = i32
     return L
 
@@ -201,6 +202,27 @@ def merge_topk(scores_g: torch.Tensor, ids_g: torch.Tensor, k: int,
                torch.empty((nq, k), dtype=torch.int64, device=scores_g.device))
     _check("uq_merge_topk", _L.uq_merge_topk(_ptr(scores_g), _ptr(ids_g), g, nq, k, _ptr(out[0]),
                                              _ptr(out[1]), _stream(stream)))
+    return out
+
+
+def rerank(q: torch.Tensor, db: torch.Tensor, cand: torch.Tensor, k: int,
+           out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
+           stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """k@n (uq_rerank): re-rank each query's candidate ids cand [nq][n] by cosine on the
+    float vectors q [nq][d] / db [N][d] (same dtype); (cos [nq][k] f32, ids [nq][k] int64)."""
+    _dev(q, "q"); _dev(db, "db"); _dev(cand, "cand")
+    if q.dtype != db.dtype or q.dtype not in _DT:
+        raise TypeError("q and db must share a supported float dtype")
+    if q.stride(1) != 1 or db.stride(1) != 1 or cand.dtype != torch.int64 or not cand.is_contiguous():
+        raise ValueError("unit column stride vectors and contiguous int64 candidates expected")
+    nq, d = q.shape
+    n_cand = cand.shape[1]
+    if out is None:
+        out = (torch.empty((nq, k), dtype=torch.float32, device=q.device),
+               torch.empty((nq, k), dtype=torch.int64, device=q.device))
+    _check("uq_rerank", _L.uq_rerank(_ptr(q), _DT[q.dtype], nq, q.stride(0), _ptr(db), db.shape[0],
+                                     db.stride(0), d, _ptr(cand), n_cand, k, _ptr(out[0]), _ptr(out[1]),
+                                     _stream(stream)))
     return out
 
 

@@ -383,6 +383,22 @@ uq_status uq_merge_topk(const int32_t* scores, const int64_t* ids, int32_t g, in
   return from_cuda(launch_merge_si(scores, ids, g, nq, k, out_scores, out_ids, (cudaStream_t)stream));
 }
 
+uq_status uq_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, const void* db, int64_t n, int64_t ld,
+                    int32_t d, const int64_t* cand, int32_t n_cand, int32_t k, float* out_cos, int64_t* out_ids,
+                    uq_stream_t stream) {
+  g_launches = 0;
+  if (nq < 0 || n < 0 || d < 1 || n_cand < 1 || k < 1 || k > n_cand || ldq < d || ld < d) return UQ_ERR_INVALID_ARG;
+  if (dt != UQ_F32 && dt != UQ_F16 && dt != UQ_BF16) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D || n_cand > UQ_MAX_K || n >= (int64_t)0xffffffff) return UQ_ERR_UNSUPPORTED;
+  if (nq == 0) return UQ_OK;
+  if (!q || !cand || !out_cos || !out_ids || (n > 0 && !db)) return UQ_ERR_INVALID_ARG;
+  const size_t es = (dt == UQ_F32) ? 4 : 2;
+  if (((uintptr_t)q % es) != 0 || (db && ((uintptr_t)db % es) != 0) || ((uintptr_t)cand % 8) != 0)
+    return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_rerank(q, dt, nq, ldq, db, n, ld, d, cand, n_cand, k, out_cos, out_ids,
+                                 (cudaStream_t)stream));
+}
+
 uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad_rows,
                          uq_stream_t stream) {
   g_launches = 0;

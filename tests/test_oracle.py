@@ -293,3 +293,30 @@ def test_cosine_knn(orc):
     assert np.allclose(2 - 2 * s, np.take_along_axis(l2, ref, 1), atol=1e-12)
     s1, i1 = orc.cosine_knn(db[5:6] * 3.0, db, 1)
     assert i1[0, 0] == 5 and abs(s1[0, 0] - 1.0) < 1e-12
+
+
+def test_rerank(orc):
+    """k@n re-rank: with every row as a candidate it is exact cosine kNN
+    (P:67-69 ranking pinned above); the candidate order does not matter; a
+    candidate subset keeps the best k of that subset; invalid ids are skipped."""
+    rng = np.random.default_rng(9)
+    db = rng.standard_normal((300, 48))
+    q = rng.standard_normal((6, 48))
+    s0, i0 = orc.cosine_knn(q, db, 12)
+    cand = np.stack([rng.permutation(300) for _ in range(6)])
+    s1, i1 = orc.rerank(q, db, cand, 12)
+    assert np.array_equal(i0, i1) and np.array_equal(s0, s1)
+    # subset: brute force over the subset by explicit unit-vector dot products
+    sub = cand[:, :40]
+    s2, i2 = orc.rerank(q, db, sub, 5)
+    for r in range(6):
+        qn = q[r] / np.linalg.norm(q[r])
+        sc = [(-float(qn @ (db[j] / np.linalg.norm(db[j]))), int(j)) for j in sub[r]]
+        best = sorted(sc)[:5]
+        assert [b[1] for b in best] == i2[r].tolist()
+        assert np.allclose([-b[0] for b in best], s2[r], atol=1e-12)
+    # padding / out-of-range ids are skipped; too few candidates pad with (-inf, -1)
+    bad = np.array([[-1, 7, 300, 3]] * 6, dtype=np.int64)
+    s3, i3 = orc.rerank(q, db, bad, 4)
+    assert (i3[:, 2:] == -1).all() and np.isinf(s3[:, 2:]).all()
+    assert all(set(i3[r, :2].tolist()) == {3, 7} for r in range(6))

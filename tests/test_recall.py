@@ -48,3 +48,66 @@ def test_cosine_gt_and_recall(uq, orc, cfg, n, nq):
     assert hits_gpu == hits
     assert abs(r_gpu - hits / (w.k * w.nq)) < 1e-6
     assert 0.05 < r_gpu < 0.9, r_gpu   # ~0.27 (c1), ~0.26 (c2)
+
+
+def _sure_mask(o_s, tol):
+    """positions whose fp64 cosine is separated from both neighbours by more than tol"""
+    gap = np.abs(np.diff(o_s, axis=1)) > tol
+    return np.concatenate([gap[:, :1], gap[:, :-1] & gap[:, 1:], gap[:, -1:]], axis=1)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("d,n_cand,k", [(768, 200, 100), (96, 37, 10), (1536, 1024, 5), (1, 3, 3)])
+def test_rerank_parity(uq, orc, dt, d, n_cand, k):
+    """uq_rerank (k@n) vs orc_rerank (fp64) on seeded random candidate
+    lists with padding / out-of-range ids: cosines within 1e-5 absolute, ids equal
+    wherever the fp64 cosines are separated by more than twice that.  Tolerance
+    (DESIGN.md §4): the kernel's fp32 dot runs d/32 sequential FMAs per lane and a
+    5-level shuffle tree, so |err| <= (d/32 + 5) u sum|q_i v_i| / (|q||v|) + norm
+    terms <= ~4e-6 for d <= 1536 (u = 2^-24, Cauchy-Schwarz) on the cosine scale."""
+    g = torch.Generator().manual_seed(d * 7 + n_cand)
+    n, nq = 3000, 17
+    db = torch.randn(n, d, generator=g).to(dt)
+    q = torch.randn(nq, d, generator=g).to(dt)
+    cand = torch.stack([torch.randperm(n, generator=g)[:n_cand] for _ in range(nq)])
+    cand[0, : n_cand // 2] = -1              # padding
+    cand[1, 0] = n + 5                       # foreign id
+    cos, ids = uq.rerank(q.cuda(), db.cuda(), cand.cuda(), k)
+    o_s, o_i = orc.rerank(q.double().numpy(), db.double().numpy(), cand.numpy(), k)
+    c = cos.double().cpu().numpy()
+    fin = np.isfinite(o_s)
+    assert np.array_equal(np.isfinite(c), fin)
+    assert np.abs(c[fin] - o_s[fin]).max() <= 1e-5
+    sure = _sure_mask(np.where(fin, o_s, -9.0), 2e-5)
+    gi = ids.cpu().numpy()
+    assert np.array_equal(gi[sure], o_i[sure])
+    assert (gi[~fin] == -1).all()
+    # every id returned is one of the query's valid candidates, without repeats
+    for r in range(nq):
+        v = [x for x in gi[r].tolist() if x >= 0]
+        assert len(set(v)) == len(v) and set(v) <= set(cand[r].tolist())
+
+
+def test_rerank_after_search_is_k_at_n(uq, orc):
+    """The paper's k@n: search the codes with n = 4k, re-rank in the float
+    space, keep k. recall@k after re-rank equals the fraction of the true top-k found
+    among the n candidates (candidates from the oracle's own kNN), and is above the
+    recall of the plain top-k search."""
+    from tools.recall import cosine_topk_fp32, recall_at_k
+    w = datagen.CONFIGS["c2"].scaled(n=40_000, nq=32)
+    db = datagen.db(w, "cuda")
+    q = datagen.queries(w, "cuda")
+    _, gt_i = cosine_topk_fp32(w, q, w.k, chunk=4096)
+    o_db = orc.pack(orc.encode(db.cpu().numpy(), w.x))
+    o_q = orc.pack(orc.encode(q.cpu().numpy(), w.x))
+    nc = 4 * w.k
+    _, o_ids = orc.knn(o_q, o_db, w.d, nc)
+    cand = torch.from_numpy(np.ascontiguousarray(o_ids)).cuda()
+    _, ids = uq.rerank(q, db, cand, w.k)
+    g = gt_i.cpu().numpy()
+    k_at_n = np.mean([len(set(a.tolist()) & set(b.tolist())) / w.k for a, b in zip(o_ids, g)])
+    r = recall_at_k(ids, gt_i)
+    r0 = recall_at_k(cand[:, : w.k], gt_i)
+    # exact up to fp32 near-ties at the k-th place: allow one id per query
+    assert abs(r - k_at_n) <= 1.0 / w.k + 1e-9, (r, k_at_n)
+    assert r > r0, (r, r0)
