@@ -228,7 +228,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(datagen.CONFIGS))
-    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc", "f4"])
     ap.add_argument("--n", type=int, default=None, help="override DB rows per GPU")
     ap.add_argument("--nq", type=int, default=None, help="override query batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -247,7 +247,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = datagen.CONFIGS[args.config].scaled(n=args.n, nq=args.nq)
-    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05}[args.algo]
+    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4}[args.algo]
     n_loc, nq, d, x, k = w.n, w.nq, w.d, w.x, w.k
     id_base = rank * n_loc
 
@@ -357,11 +357,24 @@ def main():
     peaks, peaks_src = _peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    used_tc = uq.search_resolve(nq, n_loc, d, k, algo) == uq.ALGO_TCGEN05
+    resolved = uq.search_resolve(nq, n_loc, d, k, algo)
+    used_f4 = resolved == uq.ALGO_TC_FP4
+    used_tc = resolved in (uq.ALGO_TCGEN05, uq.ALGO_TC_FP4)
+    algo_name = "tcgen05-f4" if used_f4 else "tcgen05" if used_tc else "popc"
     # dominant kernel = the main scan (every DB row); per launch: nq * n_loc Delta evaluations
     scan_avg_s = (main_ms / max(main_n, 1)) * 1e-3
     evals_per_launch = main_evals / max(main_n, 1)
-    if used_tc:
+    if used_f4:
+        # E2M1 MACs: d per Delta (T_q . T_db^T with +-1 / 0 exact in E2M1), 2 ops per MAC
+        ops = 2.0 * d * evals_per_launch
+        peak = 4.0 * float(peaks["bf16_tflops"])   # dense fp4 = 4x bf16 (9 vs 2.25 PFLOP/s nominal)
+        achieved = ops / scan_avg_s / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "scan_tc2_kernel<NB,0,1> (CTA-pair E2M1 tcgen05 kind::mxf4 Delta GEMM + fused top-k)",
+                "peak_source": f"4 x bf16_tflops of {peaks_src} MEASURED_PEAKS.json (dense fp4 = 4x bf16 nominal)",
+                "algorithmic": "2*d ops per Delta (d E2M1 MACs)"}
+    elif used_tc:
         # int8 MACs: d per Delta (the int8 GEMM T_q . T_db^T), 2 ops per MAC
         ops = 2.0 * d * evals_per_launch
         peak = 2.0 * float(peaks["bf16_tflops"])   # int8 dense = 2x bf16 (guide's nominal ratio)
@@ -397,7 +410,7 @@ def main():
                     "kernel": "scan_popc_kernel (LOP3+POPC Delta scan + fused top-k)",
                     "peak_source": f"{popc_clk:.2f} POPC/clk/SM {popc_src} x {sms} SMs x {sm_mhz:.0f} MHz",
                     "algorithmic": "2*ceil(d/32) POPC per Delta"}
-    roof["traffic"], tsrc = _traffic("tcgen05" if used_tc else "popc", w.name, nq)
+    roof["traffic"], tsrc = _traffic(algo_name, w.name, nq)
     if tsrc:
         roof["traffic_source"] = tsrc
     roof["scan_ms_avg"] = scan_avg_s * 1e3
@@ -410,10 +423,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "s8" if used_tc else "u32",
+        "scaling": "weak", "vs_baseline": None, "dtype": "e2m1" if used_f4 else "s8" if used_tc else "u32",
         "data": "synthetic",
         "config": {"workload": _workload_desc(w), "db_rows_per_gpu": n_loc, "global_db_rows": n_loc * world,
-                   "queries": nq, "k": k, "algo": "tcgen05" if used_tc else "popc",
+                   "queries": nq, "k": k, "algo": algo_name,
                    "parallelism": f"db-shard x{world} + allgather/merge" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2: {n_loc * uq.code_bytes(d) / 1e6:.0f} MB of DB codes per GPU scanned per step"},
         "qps": nq * args.steps / (ms * 1e-3),

@@ -56,7 +56,10 @@ typedef enum { UQ_F32 = 0, UQ_F16 = 1, UQ_BF16 = 2 } uq_dtype;
 typedef enum {
   UQ_ALGO_AUTO = 0,    /* tensor path for large query batches, popcount otherwise */
   UQ_ALGO_POPC = 1,    /* LOP3 + POPC scan on CUDA cores                          */
-  UQ_ALGO_TCGEN05 = 2  /* int8 tcgen05 GEMM (UTCIMMA) with fused top-k            */
+  UQ_ALGO_TCGEN05 = 2, /* int8 tcgen05 GEMM (UTCIMMA) with fused top-k            */
+  UQ_ALGO_TC_FP4 = 3   /* E2M1 tcgen05 GEMM on CTA pairs (kind::mxf4, UTCOMMA):
+                          ternary values are exact in E2M1, scales fixed at 2^0,
+                          f32 accumulation of |Delta| <= 2048 is exact; d <= 1536 */
 } uq_algo;
 
 #define UQ_MAX_D 2048
@@ -100,8 +103,8 @@ uq_status uq_search_workspace_ex(int64_t nq, int64_t n, int32_t d, int32_t k, uq
 
 /*
  * uq_search_resolve -- which scan engine uq_search_ex(algo) runs for this shape
- * on the CURRENT device (*resolved is a host pointer; UQ_ALGO_POPC or
- * UQ_ALGO_TCGEN05).  UQ_ERR_UNSUPPORTED if `algo` cannot run this shape.
+ * on the CURRENT device (*resolved is a host pointer; UQ_ALGO_POPC,
+ * UQ_ALGO_TCGEN05 or UQ_ALGO_TC_FP4).  UQ_ERR_UNSUPPORTED if `algo` cannot run this shape.
  */
 uq_status uq_search_resolve(int64_t nq, int64_t n, int32_t d, int32_t k, uq_algo algo,
                             uq_algo* resolved);

@@ -16,14 +16,14 @@ import torch
 
 __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
-    "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05",
+    "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05", "ALGO_TC_FP4",
     "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex", "rerank",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libuq.so")
 
-ALGO_AUTO, ALGO_POPC, ALGO_TCGEN05 = 0, 1, 2
+ALGO_AUTO, ALGO_POPC, ALGO_TCGEN05, ALGO_TC_FP4 = 0, 1, 2, 3
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 _STATUS = {0: "UQ_OK", 1: "UQ_ERR_INVALID_ARG", 2: "UQ_ERR_UNSUPPORTED", 3: "UQ_ERR_CUDA",
            4: "UQ_ERR_WORKSPACE"}
@@ -162,7 +162,7 @@ def search_workspace(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> 
 
 
 def search_resolve(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> int:
-    """Scan engine (ALGO_POPC / ALGO_TCGEN05) that search(algo) runs for this shape."""
+    """Scan engine (ALGO_POPC / ALGO_TCGEN05 / ALGO_TC_FP4) that search(algo) runs for this shape."""
     r = ctypes.c_int32(0)
     _check("uq_search_resolve", _L.uq_search_resolve(nq, n, d, k, algo, ctypes.byref(r)))
     return int(r.value)

@@ -68,20 +68,33 @@ static uq_status from_cuda(cudaError_t e) { return e == cudaSuccess ? UQ_OK : UQ
 // The tensor-core engine runs on CTA pairs (cta_group::2) once the query
 // batch fills a 256-query pair tile; smaller batches use the one-CTA kernel.
 static bool use_pairs(int64_t nq, int32_t d) { return nq > 128 && blocks128(d) <= 8; }
-static TcPlan plan_tc_any(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  return use_pairs(nq, d) ? plan_tc2(nq, n, d, k, sms) : plan_tc(nq, n, d, k, sms);
+static bool is_tc(uq_algo a) { return a == UQ_ALGO_TCGEN05 || a == UQ_ALGO_TC_FP4; }
+// operand kind of the CTA-pair engine that runs (a, nq, d), or -1 (no pair engine)
+static int pair_op(uq_algo a, int64_t nq, int32_t d) {
+  if (a == UQ_ALGO_TC_FP4) return 1;
+  if (a == UQ_ALGO_TCGEN05 && use_pairs(nq, d)) return 0;
+  return -1;
+}
+static TcPlan plan_tc_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  const int op = pair_op(a, nq, d);
+  return op >= 0 ? plan_tc2(nq, n, d, k, sms, op) : plan_tc(nq, n, d, k, sms);
 }
 
 // Which scan engine runs for a shape.
 static uq_algo resolve_algo(uq_algo algo, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   if (algo == UQ_ALGO_POPC) return UQ_ALGO_POPC;
-  const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
+  if (algo == UQ_ALGO_TC_FP4) return plan_tc2(nq, n, d, k, sms, 1).ok ? UQ_ALGO_TC_FP4 : UQ_ALGO_AUTO;
+  const TcPlan tp = plan_tc_for(UQ_ALGO_TCGEN05, nq, n, d, k, sms);
   if (algo == UQ_ALGO_TCGEN05) return tp.ok ? UQ_ALGO_TCGEN05 : UQ_ALGO_AUTO /* unsupported */;
   // AUTO: the popcount scan is POPC-issue-bound once nq exceeds ~3 (DESIGN.md
-  // roofline); the int8 tensor path wins for query batches that fill an M tile.
+  // roofline); the tensor paths win for query batches that fill an M tile --
+  // the E2M1 pair engine (twice the int8 MMA rate, 2.7x cheaper operand
+  // expansion) once a 256-query pair tile is more than half full.
   // small databases: the tensor engines' fixed per-CTA cost (TMEM allocation,
   // query-tile expansion, pipeline fill) exceeds a popcount scan of few rows
-  if (tp.ok && nq >= 64 && n >= ((int64_t)1 << 16)) return UQ_ALGO_TCGEN05;
+  const bool big = n >= ((int64_t)1 << 16);
+  if (nq > 128 && big && plan_tc2(nq, n, d, k, sms, 1).ok) return UQ_ALGO_TC_FP4;
+  if (tp.ok && nq >= 64 && big) return UQ_ALGO_TCGEN05;
   return UQ_ALGO_POPC;
 }
 
@@ -108,7 +121,7 @@ struct SeedPlan {
 };
 // Histogram seeding (CTA-pair tensor engine): a cheap epilogue, so a denser
 // sample (1/8) buys a tighter bound.  Top-k seeding (other engines): 1/32.
-static bool hist_seed(uq_algo a, int64_t nq, int32_t d) { return a == UQ_ALGO_TCGEN05 && use_pairs(nq, d); }
+static bool hist_seed(uq_algo a, int64_t nq, int32_t d) { return pair_op(a, nq, d) >= 0; }
 static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
   SeedPlan sp{false, 0, 1};
   static const int div_env = [] {
@@ -136,8 +149,8 @@ struct SearchLayout {
 
 static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms,
                            size_t* buf_bytes) {
-  if (a == UQ_ALGO_TCGEN05) {
-    const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
+  if (is_tc(a)) {
+    const TcPlan tp = plan_tc_for(a, nq, n, d, k, sms);
     *buf_bytes = align_up(tp.buf_bytes, 256);
     return align_up(tp.part_bytes, 256);
   }
@@ -160,8 +173,8 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   L.bufs_off = 0;
   L.part_off = bufs;
   L.cnt_off = L.part_off + part;      // [lists][nq] valid entries per list (pair engine)
-  const size_t cnt_bytes = (a == UQ_ALGO_TCGEN05 && use_pairs(nq, d))
-                               ? align_up((size_t)plan_tc2(nq, n, d, k, sms).n_chunks * nq * 4, 256) : 0;
+  const int op = pair_op(a, nq, d);
+  const size_t cnt_bytes = op >= 0 ? align_up((size_t)plan_tc2(nq, n, d, k, sms, op).n_chunks * nq * 4, 256) : 0;
   L.seed_s_off = L.cnt_off + cnt_bytes;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
   L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * (hist ? 1 : k) * 4, 256) : 0);
   L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
@@ -183,10 +196,11 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   int64_t lists = 0;
   cudaError_t e;
   timer_begin(st, &ev, timer_kind, (double)nq * (double)n);
-  if (a == UQ_ALGO_TCGEN05) {
-    const TcPlan tp = plan_tc_any(nq, n, d, k, sms);
-    e = use_pairs(nq, d) ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, st)
-                      : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
+  const int op = pair_op(a, nq, d);
+  if (is_tc(a)) {
+    const TcPlan tp = plan_tc_for(a, nq, n, d, k, sms);
+    e = op >= 0 ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, op, st)
+                : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
     lists = tp.n_chunks;
   } else {
     const PopcPlan pl = plan_popc(nq, n, d, k, sms);
@@ -196,8 +210,8 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   timer_end(st, ev);
   if (e != cudaSuccess) return e;
   // the pair engine publishes variable-length lists of up to cap entries with counts
-  const bool counted = a == UQ_ALGO_TCGEN05 && use_pairs(nq, d);
-  const int32_t kin = counted ? plan_tc2(nq, n, d, k, sms).cap : k;
+  const bool counted = op >= 0;
+  const int32_t kin = counted ? plan_tc2(nq, n, d, k, sms, op).cap : k;
   return launch_merge_keys(part, lists, nq, kin, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr);
 }
 
@@ -347,7 +361,8 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     if (cudaMemsetAsync(ghist, 0, (size_t)nq * 128 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)sp.rows);
-    cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, sp.stride, ghist, thr, sms, st);
+    cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, sp.stride, ghist, thr, sms,
+                                         pair_op(a, nq, d), st);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = thr;

@@ -195,5 +195,11 @@ __device__ __forceinline__ uint32_t stream_rebuild(uint32_t* buf, int cnt, int k
 __device__ __forceinline__ uint32_t ordered_rebuild(uint32_t* buf, int cnt, int k, int lane, int rb) {
   UQ_REBUILD_DISPATCH(ordered_rebuild_regs, buf, cnt, k, lane, rb);
 }
+// Out-of-line form for kernels whose hot loops must stay small in the
+// instruction cache (the five inlined MAXR variants are ~5k SASS instructions;
+// the call is rare: about one cut per stream)
+static __device__ __noinline__ uint32_t ordered_rebuild_call(uint32_t* buf, int cnt, int k, int lane, int rb) {
+  UQ_REBUILD_DISPATCH(ordered_rebuild_regs, buf, cnt, k, lane, rb);
+}
 
 }  // namespace uq

@@ -56,16 +56,17 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                            cudaStream_t st);
 
-// Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128.
-TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+// Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128;
+// op: operand kind, 0 = int8 (kind::i8), 1 = E2M1 (kind::mxf4, f32 accumulate).
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op);
 cudaError_t tc2_prof_read(unsigned long long* out48);
-TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
+TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op);
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
-                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms,
+                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms, int op,
                                  cudaStream_t st);
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
-                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
+                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st);
 
 }  // namespace uq

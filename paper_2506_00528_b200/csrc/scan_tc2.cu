@@ -48,19 +48,35 @@ namespace tc2 {
 using namespace ::uq::tc;
 
 constexpr int BM = 128;               // queries per CTA (pair M = 256)
-constexpr int BN = 256;               // DB rows per pair tile (UMMA N)
-constexpr int BH = BN / 2;            // DB rows expanded per CTA (128: four producer warps)
-constexpr int KB = 128;               // dims per expansion block (one uint4 of each plane)
-constexpr int kBlkPerStage = 2;       // 256 dims per pipeline stage
 constexpr int kProdWarps = 4;         // warps 0-3
 constexpr int kMmaWarp = 3;           // warp 3: also MMA issuer (leader) + TMEM owner
 constexpr int kEpiSets = 2;           // epilogue warp sets, each owns half of a tile's columns
 constexpr int kEpiWarp0 = 4;          // warps 4..11 (warp % 4 = TMEM lane quarter)
 constexpr int kThreads = (kProdWarps + 4 * kEpiSets) * 32;  // 12 warps: 3 per SMSP -> 168 regs
-constexpr int kAccStride = 256;       // TMEM column offset of the second accumulator
-constexpr int kBlkBytes = BH * KB;    // 16 KB per CTA per 128-dim block
-constexpr int kStageBytes = kBlkPerStage * kBlkBytes;  // 32 KB
-constexpr uint32_t kTmemCols = 512;   // two s32 accumulators (columns 0 and 256)
+constexpr uint32_t kTmemCols = 512;   // two accumulators (+ the f4 scale factors)
+constexpr int kOpI8 = 0, kOpF4 = 1;   // operand kind: int8 (kind::i8) / E2M1 (kind::mxf4)
+
+// Tile geometry per operand kind.
+//   i8: N = 256 rows per pair tile (128 per CTA), 128 B of SMEM per row per
+//       128-dim block, two 256-column s32 accumulators fill TMEM;
+//   f4: N = 240 (120 per CTA): two 240-column f32 accumulators leave TMEM
+//       columns [480, 512) for the (constant) scale factors; 64 B per row per
+//       block, so a stage of 3-4 blocks (384-512 dims) still carries 6-8 MMAs.
+template <int OP> struct Geo {
+  static constexpr int BN = OP == kOpF4 ? 240 : 256;   // UMMA N
+  static constexpr int BH = BN / 2;                    // DB rows expanded per CTA
+  static constexpr int RB = OP == kOpF4 ? 64 : 128;    // SMEM bytes per row per 128-dim block
+  static constexpr int CPB = RB / 16;                  // 16-B K chunks per block
+  static constexpr int MPB = RB / 32;                  // MMAs per block (32 B of K each)
+  static constexpr int ACC = BN;                       // TMEM column of the second accumulator
+  static constexpr uint32_t SF_COL = 480;              // f4 scale factors: columns [480, 512)
+  static constexpr int CW = BN / kEpiSets;             // accumulator columns per epilogue set
+  static constexpr int bps(int NB) {                   // 128-dim blocks per pipeline stage
+    return OP == kOpI8 ? 2 : (NB <= 4 ? NB : (NB + (NB + 3) / 4 - 1) / ((NB + 3) / 4));
+  }
+  static constexpr int stage_bytes(int NB) { return bps(NB) * BH * RB; }
+};
+constexpr int kF4Bias = 0x4B400000;   // f32 bits of 1.5 * 2^23: (float)(v) + 1.5*2^23 has bits kF4Bias + v
 constexpr int kHistBins = 128;
 constexpr int kHistBytes = (kHistBins / 2) * BM * 4;   // [64 words][128 queries], two u16 counts per word
 constexpr int kModeTopK = 0, kModeHist = 1;
@@ -107,6 +123,7 @@ struct Item {
   int64_t row0, rows;
 };
 
+template <int BN>
 __device__ __forceinline__ Item decode_item(const Params& p, int64_t i) {
   Item it;
   const int64_t big = (int64_t)p.r_hi * (p.s_lo + 1);
@@ -142,17 +159,26 @@ __device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* 
   }
 }
 
-template <int NB, int MODE>
+template <int NB, int MODE, int OP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc2_kernel(Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int KTOT = NB * KB;
+  using G = Geo<OP>;
+  constexpr int BN = G::BN, BH = G::BH;
+  constexpr int kBlkPerStage = G::bps(NB);
+  constexpr int kStageBytes = G::stage_bytes(NB);
+  constexpr int kAccStride = G::ACC;
   constexpr int NST = (NB + kBlkPerStage - 1) / kBlkPerStage;  // stages per tile
   constexpr uint32_t A_LBO = BM * 16;   // next 16-B K chunk of A (128 rows)
   constexpr uint32_t B_LBO = BH * 16;   // next 16-B K chunk of this CTA's B half
   constexpr uint32_t SBO = 128;         // next 8-row group
+  // scores: i8 accumulators are s32.  f4 accumulators are f32 holding exact
+  // integers; a warp whose thresholds t are all >= 0 compares the raw f32
+  // bits as int32 (for t >= 0, v > t as floats <=> bits(v) > bits(t) as
+  // int32: negative floats and -0.0 have negative bit patterns), otherwise it
+  // first adds 1.5*2^23 (bits kF4Bias + v, one FADD per score).
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)BM * KTOT;
+  uint8_t* sB = smem + (size_t)BM * NB * G::RB;
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(sB + (size_t)p.stages * kStageBytes);  // kHist only
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(s_hist) + (MODE == kModeHist ? kHistBytes : 0));
   uint64_t* full = bars;                   // [stages] (leader): 2 CTAs x producer warps
@@ -187,18 +213,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
+  if (OP == kOpF4 && warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+    // UE8M0 scale factors = 2^0 (0x7F) in every byte of columns [480, 512): the
+    // MMA's SFA / SFB reads fall inside, whatever their layout
+    const uint32_t ta = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + G::SF_COL;
+    tmem_fill16(ta, 0x7F7F7F7Fu);
+    tmem_fill16(ta + 16u, 0x7F7F7F7Fu);
+    tc_fence_before();   // ordered before the MMAs by the item's cluster_sync below
+  }
   const long long t_setup = PROF_ON ? clk() : 0;
   if (threadIdx.x == 0) PROF_ADD(11, t_setup - t_entry);
 
   int stage = 0;            // producers: next stage to fill
   uint32_t sphase = 0;
-  int mstage = 0;           // MMA issuer: next stage to consume
-  uint32_t mphase = 0;
   int acc = 0;              // accumulator buffer (issuer and epilogue each track it)
   uint32_t aphase = 0;
 
   for (int64_t item = pair; item < p.n_items; item += npairs) {
-    const Item it = decode_item(p, item);
+    const Item it = decode_item<BN>(p, item);
     const int64_t q0 = (int64_t)it.t * (2 * BM) + (int64_t)cr * BM;  // this CTA's queries
     const int64_t row0 = it.row0;
     const int64_t rows = it.rows;
@@ -214,7 +246,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
         qp = *reinterpret_cast<const uint4*>(src);
         qn = *reinterpret_cast<const uint4*>(src + pb);
       }
-      expand_block_store(qp, qn, sA + (size_t)(kb * 8) * A_LBO + (r >> 3) * SBO + (r & 7) * 16, A_LBO);
+      uint8_t* dst = sA + (size_t)(kb * G::CPB) * A_LBO + (r >> 3) * SBO + (r & 7) * 16;
+      if (OP == kOpF4) expand_block_store_f4(qp, qn, dst, A_LBO);
+      else expand_block_store(qp, qn, dst, A_LBO);
     }
     fence_proxy_async();
     cluster_sync();  // both CTAs' A tiles are in place before the leader issues
@@ -240,7 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       };
       auto load_block = [&](int tile, int kb, uint4& a, uint4& b) {
         const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + r;
-        if (tile < ntiles && lr < rows && !(p.dbg & 4)) {
+        if (tile < ntiles && lr < rows && r < BH && !(p.dbg & 4)) {
           const uint8_t* src = p.db + sample_row(row0 + lr) * cb;
           a = __ldg(reinterpret_cast<const uint4*>(src) + kb);
           b = __ldg(reinterpret_cast<const uint4*>(src + pb) + kb);
@@ -256,13 +290,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       // the register ring hides one tile of latency, L2 covers the rest
       auto prefetch_rows = [&](int tile) {
         const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + (r & ~31);
-        if ((MODE == kModeHist || p.row_stride == 1) && lane == 0 && tile < ntiles && lr < rows) {
-          const int64_t nr = (rows - lr < 32) ? rows - lr : 32;   // 32 rows stay inside one BN-row block
+        if ((MODE == kModeHist || p.row_stride == 1) && lane == 0 && tile < ntiles && lr < rows &&
+            (r & ~31) < BH) {
+          int64_t nr = (rows - lr < 32) ? rows - lr : 32;   // 32 rows stay inside one BN-row block
+          if (nr > BH - (r & ~31)) nr = BH - (r & ~31);
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.db + sample_row(row0 + lr) * cb),
                        "r"((uint32_t)(nr * cb)) : "memory");
         }
       };
-      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      constexpr uint32_t idesc = OP == kOpF4 ? idesc_mxf4(2 * BM, BN) : idesc_i8(2 * BM, BN);
+      const uint32_t sf_tmem = tmem_base + G::SF_COL;
       const uint64_t a_desc0 = smem_desc(smem_u32(sA), A_LBO, SBO);
       const uint64_t b_desc0 = smem_desc(smem_u32(sB), B_LBO, SBO);
       prefetch_rows(1);
@@ -279,8 +316,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           for (int bb = 0; bb < kBlkPerStage; ++bb) {
             const int kb = ks * kBlkPerStage + bb;
             if (kb < NB) {
-              if (!(p.dbg & 1))
-                expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * 8) * B_LBO, B_LBO, !(p.dbg & 32));
+              if (!(p.dbg & 1) && r < BH) {
+                if (OP == kOpF4)
+                  expand_block_store_f4(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(p.dbg & 32));
+                else
+                  expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(p.dbg & 32));
+              }
               load_block(tile + 1, kb, dp[kb], dn[kb]);
             }
           }
@@ -304,10 +345,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
                 const int kb = ks * kBlkPerStage + bb;
                 if (kb < NB) {
 #pragma unroll
-                  for (int kk = 0; kk < KB / 32; ++kk) {
-                    const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)(kb * 8 + kk * 2) * A_LBO) >> 4);
-                    const uint64_t bd = b_stage + (uint64_t)(((uint32_t)(bb * 8 + kk * 2) * B_LBO) >> 4);
-                    mma2_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                  for (int kk = 0; kk < G::MPB; ++kk) {
+                    const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)(kb * G::CPB + kk * 2) * A_LBO) >> 4);
+                    const uint64_t bd = b_stage + (uint64_t)(((uint32_t)(bb * G::CPB + kk * 2) * B_LBO) >> 4);
+                    if (OP == kOpF4) mma2_f4(d_tmem, ad, bd, idesc, sf_tmem, sf_tmem, (kb | kk) != 0 ? 1u : 0u);
+                    else mma2_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                   }
                 }
               }
@@ -338,7 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       const int col = quarter * 32 + lane;    // this thread's query inside the CTA tile
       const int64_t qme = q0 + col;
       const uint32_t tempty_dst = mapa(smem_u32(&tempty[0]), 0);  // leader's tempty[0]
-      constexpr int CW = BN / kEpiSets;       // columns per set per tile
+      constexpr int CW = G::CW;               // columns per set per tile
       if (MODE == kModeHist) {
         // Only Delta >= F enters the histogram, F = z nnz(q) / sqrt(d) (z standard
         // deviations of Delta against unrelated codes, z chosen on the host so
@@ -356,6 +398,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           }
           floor_m1 = max(0, (int)(p.zfloor * (float)nnz * rsqrtf((float)p.d))) - 1;
         }
+        const bool raw = OP == kOpF4 && __all_sync(kFull, floor_m1 >= 0);
+        const int fl = OP != kOpF4 ? floor_m1 : raw ? __float_as_int((float)floor_m1) : min(floor_m1, 4096) + kF4Bias;
+        const uint32_t pad = (OP == kOpF4 && !raw) ? 0u : 0x80000000u;
         for (int tile = 0; tile < ntiles; ++tile) {
           mbar_wait(smem_u32(&tfull[acc]), aphase);
           tc_fence_after();
@@ -367,26 +412,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + (uint32_t)c0, v);
-            if (ncols - c0 < 32) {
+            if (OP == kOpF4 && !raw) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (c0 + j >= ncols) v[j] = 0x80000000u;
+              for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 12582912.0f);
             }
+            // 4-score maxima, one vote for the whole 32-score row; then, per
+            // 4-score chunk some lane needs, a register-only append
             int cm[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
-            const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
-                                        max(cm[6], cm[7]));
-            if (__any_sync(kFull, mx > floor_m1)) {
+            if (ncols - c0 < 32) {
+              // columns past the tile: whole 4-groups masked at the maxima (f4's
+              // 120-column sets end on a group boundary), element-wise only in a
+              // database's partial last group
+              const int rem = ncols - c0;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                if (__any_sync(kFull, cm[i] > floor_m1)) {
+                if (4 * i >= rem) {
+                  cm[i] = (int)pad;
+                } else if (4 * i + 4 > rem) {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    if (4 * i + j >= rem) v[4 * i + j] = pad;
+                  cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
+                }
+              }
+            }
+            const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
+                                        max(cm[6], cm[7]));
+            if (__any_sync(kFull, mx > fl)) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (__any_sync(kFull, cm[i] > fl)) {
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const int sc = (int)v[4 * i + j];
-                    if (sc > floor_m1) {
-                      const uint32_t b = min((uint32_t)sc >> p.hshift, (uint32_t)(kHistBins - 1));
+                    if (sc > fl) {
+                      const int dv = OP != kOpF4 ? sc : raw ? __float2int_rn(__int_as_float(sc)) : sc - kF4Bias;
+                      const uint32_t b = min((uint32_t)dv >> p.hshift, (uint32_t)(kHistBins - 1));
                       atomicAdd(s_hist + (b >> 1) * BM + col, (b & 1u) ? 0x10000u : 1u);
                     }
                   }
@@ -422,6 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           const int32_t dk = p.thr0[qme * p.thr0_stride];
           if (dk != INT32_MIN) thrd = dk - 1;
         }
+
         long long t_loop = PROF_ON ? clk() : 0, t_w = 0, t_f = 0, t_r = 0;
         for (int tile = 0; tile < ntiles; ++tile) {
           long long t0 = PROF_ON ? clk() : 0;
@@ -432,15 +497,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           const uint32_t tbase =
               tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kAccStride) + (uint32_t)(h * CW);
           const int64_t lr0 = (int64_t)tile * BN + h * CW;  // local row of this set's column 0
+          // f4 compare form for this tile (biased form: |Delta| <= 2048, so max(thrd, -4096) loses nothing)
+          const bool raw = OP == kOpF4 && __all_sync(kFull, thrd >= 0);
+          const int thb = OP != kOpF4 ? thrd : raw ? __float_as_int((float)thrd) : max(thrd, -4096) + kF4Bias;
+          const uint32_t pad = (OP == kOpF4 && !raw) ? 0u : 0x80000000u;
           const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
 #pragma unroll 1
           for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + (uint32_t)c0, v);
-            if (ncols - c0 < 32) {
+            if (OP == kOpF4 && !raw) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (c0 + j >= ncols) v[j] = 0x80000000u;
+              for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 12582912.0f);
             }
             // 4-score maxima, one vote for the whole 32-score row; then, per
             // 4-score chunk some lane needs, a register-only append
@@ -448,17 +516,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
+            if (ncols - c0 < 32) {
+              // columns past the tile: whole 4-groups masked at the maxima (f4's
+              // 120-column sets end on a group boundary), element-wise only in a
+              // database's partial last group
+              const int rem = ncols - c0;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (4 * i >= rem) {
+                  cm[i] = (int)pad;
+                } else if (4 * i + 4 > rem) {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    if (4 * i + j >= rem) v[4 * i + j] = pad;
+                  cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
+                }
+              }
+            }
             const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                         max(cm[6], cm[7]));
-            if (__any_sync(kFull, mx > thrd)) {
+            if (__any_sync(kFull, mx > thb)) {
               const uint32_t rb0 = (uint32_t)(lr0 + c0);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                if (__any_sync(kFull, cm[i] > thrd)) {
+                if (__any_sync(kFull, cm[i] > thb)) {
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const int sc = (int)v[4 * i + j];
-                    if (sc > thrd) { my_buf[cnt++] = local_key(p.kf, sc, rb0 + (uint32_t)(4 * i + j)); ++n_app; }
+                    if (sc > thb) {
+                      const int dv = OP != kOpF4 ? sc : raw ? __float2int_rn(__int_as_float(sc)) : sc - kF4Bias;
+                      my_buf[cnt++] = local_key(p.kf, dv, rb0 + (uint32_t)(4 * i + j));
+                      ++n_app;
+                    }
                   }
                 }
               }
@@ -475,7 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
             const int L = __ffs(need) - 1;
             need &= need - 1;
             const int cL = __shfl_sync(kFull, cnt, L);
-            const uint32_t D = ordered_rebuild(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
+            const uint32_t D = ordered_rebuild_call(wbufs + (size_t)L * p.cap, cL, p.k, lane, p.kf.rb);
             if (lane == L) {
               cnt = p.k;
               thrd = max(thrd, (int)D - p.kf.off);
@@ -591,13 +680,15 @@ __global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, int
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+template <int OP>
 static int tc2_stages(int NB, int mode) {
-  const int a_bytes = tc2::BM * NB * tc2::KB;
+  const int a_bytes = tc2::BM * NB * tc2::Geo<OP>::RB;
   const int budget = 227 * 1024 - a_bytes - (mode == tc2::kModeHist ? tc2::kHistBytes : 0) - 2048;
-  int s = budget / tc2::kStageBytes;
+  int s = budget / tc2::Geo<OP>::stage_bytes(NB);
   if (s > 6) s = 6;
   return s;
 }
+static int tc2_max_nb(int op) { return op == tc2::kOpF4 ? 12 : 8; }
 
 static int tc2_hist_shift(int32_t d) {
   int hs = bitlen((uint32_t)d) - 7;  // (d >> hs) < 128
@@ -606,21 +697,23 @@ static int tc2_hist_shift(int32_t d) {
 
 // Pairs: the query set is cut into 256-query pair tiles; each of the SMs/2
 // pairs gets one (pair tile, DB chunk) item when the tiles do not cover them.
+template <int OP>
 static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int mode) {
+  using G = tc2::Geo<OP>;
   TcPlan pl{};
   const int NB = blocks128(d);
   pl.ok = false;
-  if (NB > 8 || nq < 1 || n < 1) return pl;
-  pl.stages = tc2_stages(NB, mode);
+  if (NB > tc2_max_nb(OP) || nq < 1 || n < 1) return pl;
+  pl.stages = tc2_stages<OP>(NB, mode);
   if (pl.stages < 2) return pl;
   pl.ok = true;
   const int npairs = sms / 2;
   pl.n_qtiles = (int32_t)((nq + 2 * tc2::BM - 1) / (2 * tc2::BM));
-  pl.cap = k + 2 * (tc2::BN / tc2::kEpiSets);
+  pl.cap = k + 2 * G::CW;
   const KeyFmt kf = make_keyfmt(d);
-  const int64_t lmax = ((int64_t)kf.rmask + 1) / tc2::BN * tc2::BN;
+  const int64_t lmax = ((int64_t)kf.rmask + 1) / G::BN * G::BN;
   const int64_t s_min = (n + lmax - 1) / lmax;
-  int64_t s_cap = (n + 4 * tc2::BN - 1) / (4 * tc2::BN);
+  int64_t s_cap = (n + 4 * G::BN - 1) / (4 * G::BN);
   if (s_cap < s_min) s_cap = s_min;
   const int64_t QT = pl.n_qtiles;
   if (QT * s_min >= npairs) {
@@ -637,48 +730,64 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   pl.n_items = QT * pl.s_lo + pl.r_hi;
   const int64_t pairs = pl.n_items < npairs ? pl.n_items : npairs;
   pl.grid = (int32_t)(2 * pairs);
-  pl.smem = 1024 + tc2::BM * NB * tc2::KB + pl.stages * tc2::kStageBytes +
+  pl.smem = 1024 + tc2::BM * NB * G::RB + pl.stages * G::stage_bytes(NB) +
             (mode == tc2::kModeHist ? tc2::kHistBytes : 0) + (2 * pl.stages + 4) * 8 + 16;
   pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * tc2::kEpiSets * tc2::BM * pl.cap * 4;
   pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * pl.cap * 8;
   return pl;
 }
 
-TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  return plan_tc2_mode(nq, n, d, k, sms, tc2::kModeTopK);
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op) {
+  return op == tc2::kOpF4 ? plan_tc2_mode<tc2::kOpF4>(nq, n, d, k, sms, tc2::kModeTopK)
+                          : plan_tc2_mode<tc2::kOpI8>(nq, n, d, k, sms, tc2::kModeTopK);
 }
-TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  return plan_tc2_mode(nq, n, d, k, sms, tc2::kModeHist);
+TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op) {
+  return op == tc2::kOpF4 ? plan_tc2_mode<tc2::kOpF4>(nq, n, d, k, sms, tc2::kModeHist)
+                          : plan_tc2_mode<tc2::kOpI8>(nq, n, d, k, sms, tc2::kModeHist);
 }
 
-template <int NB, int MODE>
+template <int NB, int MODE, int OP>
 static cudaError_t launch_tc2_nb(const tc2::Params& p, const TcPlan& pl, cudaStream_t st) {
-  auto kern = tc2::scan_tc2_kernel<NB, MODE>;
+  auto kern = tc2::scan_tc2_kernel<NB, MODE, OP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
   kern<<<pl.grid, tc2::kThreads, pl.smem, st>>>(p);
   note_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess && getenv("UQ_DEBUG"))
-    fprintf(stderr, "scan_tc2_kernel<%d,%d> launch (grid %d, smem %d): %s\n", NB, MODE, pl.grid, pl.smem,
+    fprintf(stderr, "scan_tc2_kernel<%d,%d,%d> launch (grid %d, smem %d): %s\n", NB, MODE, OP, pl.grid, pl.smem,
             cudaGetErrorString(e));
   return e;
 }
 
-template <int MODE>
-static cudaError_t launch_tc2_mode(const tc2::Params& p, const TcPlan& pl, int NB, cudaStream_t st) {
+template <int MODE, int OP>
+static cudaError_t launch_tc2_op(const tc2::Params& p, const TcPlan& pl, int NB, cudaStream_t st) {
   switch (NB) {
-    case 1: return launch_tc2_nb<1, MODE>(p, pl, st);
-    case 2: return launch_tc2_nb<2, MODE>(p, pl, st);
-    case 3: return launch_tc2_nb<3, MODE>(p, pl, st);
-    case 4: return launch_tc2_nb<4, MODE>(p, pl, st);
-    case 5: return launch_tc2_nb<5, MODE>(p, pl, st);
-    case 6: return launch_tc2_nb<6, MODE>(p, pl, st);
-    case 7: return launch_tc2_nb<7, MODE>(p, pl, st);
-    case 8: return launch_tc2_nb<8, MODE>(p, pl, st);
+    case 1: return launch_tc2_nb<1, MODE, OP>(p, pl, st);
+    case 2: return launch_tc2_nb<2, MODE, OP>(p, pl, st);
+    case 3: return launch_tc2_nb<3, MODE, OP>(p, pl, st);
+    case 4: return launch_tc2_nb<4, MODE, OP>(p, pl, st);
+    case 5: return launch_tc2_nb<5, MODE, OP>(p, pl, st);
+    case 6: return launch_tc2_nb<6, MODE, OP>(p, pl, st);
+    case 7: return launch_tc2_nb<7, MODE, OP>(p, pl, st);
+    case 8: return launch_tc2_nb<8, MODE, OP>(p, pl, st);
     default: break;
   }
+  if (OP == tc2::kOpF4) {
+    switch (NB) {
+      case 9: return launch_tc2_nb<9, MODE, tc2::kOpF4>(p, pl, st);
+      case 10: return launch_tc2_nb<10, MODE, tc2::kOpF4>(p, pl, st);
+      case 11: return launch_tc2_nb<11, MODE, tc2::kOpF4>(p, pl, st);
+      case 12: return launch_tc2_nb<12, MODE, tc2::kOpF4>(p, pl, st);
+      default: break;
+    }
+  }
   return cudaErrorInvalidValue;
+}
+template <int MODE>
+static cudaError_t launch_tc2_mode(const tc2::Params& p, const TcPlan& pl, int NB, int op, cudaStream_t st) {
+  return op == tc2::kOpF4 ? launch_tc2_op<MODE, tc2::kOpF4>(p, pl, NB, st)
+                          : launch_tc2_op<MODE, tc2::kOpI8>(p, pl, NB, st);
 }
 
 static int tc2_dbg() {
@@ -699,21 +808,21 @@ cudaError_t tc2_prof_read(unsigned long long* out48) {
 
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
-                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
+                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st) {
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
                 thr0_stride, row_stride, nullptr, 0, 0.f, tc2_dbg()};
-  return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), st);
+  return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
 
 // Threshold seeding over rows {i * row_stride : i < n}: histogram scan, then
 // thr[q] (stride 1) from the histogram.  ghist: [nq][128] u32, zero on entry
 // (left zero on exit).
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
-                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms,
+                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms, int op,
                                  cudaStream_t st) {
-  const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms);
+  const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;
   const int hs = tc2_hist_shift(d);
   // floor: about 4k of n unrelated rows exceed it (Gaussian tail), z in [0, 4]
@@ -724,7 +833,7 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
                 nullptr, 0, row_stride, ghist, hs, z, tc2_dbg()};
-  cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), st);
+  cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, k, hs, thr);
   note_launch();

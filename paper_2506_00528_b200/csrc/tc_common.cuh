@@ -113,6 +113,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "memory");
 }
 
+// 64 accumulator columns (one .x64 load, then wait) -- halves the number of
+// exposed TMEM load latencies per tile against two x32 loads
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+      : "r"(taddr)
+      : "memory");
+}
+
 // Shared-memory matrix descriptor, K-major, SWIZZLE_NONE: core matrices are
 // 8 rows x 16 B (128 contiguous bytes); lbo = byte stride between core
 // matrices along K, sbo = byte stride between 8-row groups along M/N.
@@ -241,6 +253,61 @@ __device__ __forceinline__ void mma2_i8(uint32_t d_tmem, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// D[tmem] (+)= A . B^T over a CTA pair, E2M1 x E2M1 -> f32 with UE8M0 block-32
+// scale factors read from TMEM (sfa / sfb: TMEM addresses; all scales 2^0 here)
+__device__ __forceinline__ void mma2_f4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t sfa, uint32_t sfb, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+// Instruction descriptor of kind::mxf4: A, B E2M1 (MXF4 format 1), UE8M0 scale
+// factors (bit 23), K-major, dense K = 64, M x N.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+  return (1u << 7)                        // A: E2M1
+         | (1u << 10)                     // B: E2M1
+         | ((uint32_t)(N >> 3) << 17)     // N / 8
+         | (1u << 23)                     // scale factors UE8M0
+         | ((uint32_t)(M >> 4) << 24);    // M / 16
+}
+// 16 columns of this warp's TMEM lane quarter := v (then wait for the stores)
+__device__ __forceinline__ void tmem_fill16(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n\t"
+      "tcgen05.wait::st.sync.aligned;" ::"r"(taddr), "r"(v)
+      : "memory");
+}
+
+// 32 dims (one 32-bit word of each plane) -> 4 words of E2M1 nibbles (+1 ->
+// 0x2, -1 -> 0xA, 0 -> 0x0).  Nibble j of output word t holds dim 4j + t, so
+// chunk byte 4t + j/2 (nibble j%2) <-> dim 4j + t: A and B use the same
+// permutation of K, which leaves every dot product unchanged.  15 ALU ops per
+// 32 dims (the int8 expansion: 40).
+__device__ __forceinline__ void expand_word_f4(uint32_t p, uint32_t n, uint32_t (&o)[4]) {
+  const uint32_t m = p | n;   // |v| = 1
+  o[0] = ((m << 1) & 0x22222222u) | ((n << 3) & 0x88888888u);
+  o[1] = (m & 0x22222222u) | ((n << 2) & 0x88888888u);
+  o[2] = ((m >> 1) & 0x22222222u) | ((n << 1) & 0x88888888u);
+  o[3] = ((m >> 2) & 0x22222222u) | (n & 0x88888888u);
+}
+// One 128-dim block of one row -> 4 chunks of 16 B (E2M1) at base + c * chunk_stride.
+__device__ __forceinline__ void expand_block_store_f4(uint4 p, uint4 n, uint8_t* base, uint32_t chunk_stride,
+                                                      bool store = true) {
+  const uint32_t pw[4] = {p.x, p.y, p.z, p.w};
+  const uint32_t nw[4] = {n.x, n.y, n.z, n.w};
+  const uint32_t sbase = smem_u32(base);
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t o[4];
+    expand_word_f4(pw[w], nw[w], o);
+    if (store) st_shared_v4(sbase + w * chunk_stride, o[0], o[1], o[2], o[3]);
+    else asm volatile("" ::"r"(o[0] ^ o[1] ^ o[2] ^ o[3]));
+  }
+}
+
 // commit the issuing thread's prior tcgen05 ops to the barrier at the same
 // shared offset in every CTA of `mask`
 __device__ __forceinline__ void mma2_commit_mc(uint32_t bar, uint16_t mask) {

@@ -12,7 +12,7 @@ import datagen
 
 pytestmark = pytest.mark.gpu
 
-ALGOS = ("popc", "tc")
+ALGOS = ("popc", "tc", "f4")
 
 
 @pytest.fixture(scope="module")
@@ -26,12 +26,12 @@ def uq():
 
 
 def _algo(uq, name):
-    return {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "auto": uq.ALGO_AUTO}[name]
+    return {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4, "auto": uq.ALGO_AUTO}[name]
 
 
-def _tc_supported(uq, nq, n, d, k):
+def _tc_supported(uq, nq, n, d, k, algo=None):
     try:
-        uq.search_workspace(nq, n, d, k, uq.ALGO_TCGEN05)
+        uq.search_workspace(nq, n, d, k, uq.ALGO_TCGEN05 if algo is None else algo)
         return True
     except uq.UQError:
         return False
@@ -155,7 +155,7 @@ def _search_case(uq, orc, algo, d, x, n, nq, k, seed=0, mode="normal"):
     o_db = orc.pack(orc.encode(u_db, x)) if n else np.zeros((0, 2 * orc.plane_bytes(d)), np.uint8)
     o_q = orc.pack(orc.encode(u_q, x))
     a = _algo(uq, algo)
-    if algo == "tc" and not _tc_supported(uq, nq, n, d, k):
+    if algo in ("tc", "f4") and not _tc_supported(uq, nq, n, d, k, a):
         pytest.skip("tcgen05 path does not support this shape")
     s, i = uq.search(torch.from_numpy(o_q).cuda(), torch.from_numpy(o_db).cuda(), d, k,
                      id_base=5, algo=a)
@@ -180,10 +180,11 @@ def test_search_parity_dims(uq, orc, algo, d, x):
     _search_case(uq, orc, algo, d, x, 6000, 150, 10, seed=d)
 
 
-def test_search_parity_large_k_pairs(uq, orc):
-    """Pair engine with k = 1000: counted candidate lists larger than the merge's
+@pytest.mark.parametrize("algo", ["tc", "f4"])
+def test_search_parity_large_k_pairs(uq, orc, algo):
+    """Pair engines with k = 1000: counted candidate lists larger than the merge's
     shared-memory stage (its global-memory fallback) and many in-loop cuts."""
-    _search_case(uq, orc, "tc", 384, 192, 300_000, 200, 1000, seed=77, mode="dup")
+    _search_case(uq, orc, algo, 384, 192, 300_000, 200, 1000, seed=77, mode="dup")
 
 
 @pytest.mark.parametrize("algo", ALGOS)
@@ -219,7 +220,7 @@ def test_search_c1_full(uq, orc, algo):
     o_q = orc.pack(orc.encode(q.cpu().numpy(), w.x))
     assert np.array_equal(dbc.cpu().numpy(), o_db) and np.array_equal(qc.cpu().numpy(), o_q)
     assert np.array_equal(uq.scores(qc, dbc, w.d).cpu().numpy(), orc.scores(o_q, o_db, w.d))
-    if algo == "tc" and not _tc_supported(uq, w.nq, w.n, w.d, w.k):
+    if algo in ("tc", "f4") and not _tc_supported(uq, w.nq, w.n, w.d, w.k, _algo(uq, algo)):
         pytest.skip("tcgen05 path does not support this shape")
     s, i = uq.search(qc, dbc, w.d, w.k, algo=_algo(uq, algo))
     s_ref, i_ref = orc.knn(o_q, o_db, w.d, w.k)
@@ -280,7 +281,7 @@ def test_sharded_equals_unsharded(uq, orc, algo, G):
     codes = uq.encode(u, x)
     db, q = codes[:n], codes[n:]
     a = _algo(uq, algo)
-    if algo == "tc" and not _tc_supported(uq, nq, n // G, d, k):
+    if algo in ("tc", "f4") and not _tc_supported(uq, nq, n // G, d, k, a):
         pytest.skip("tcgen05 path does not support this shape")
     s0, i0 = uq.search(q, db, d, k, algo=a)
     bounds = np.linspace(0, n, G + 1).astype(int)

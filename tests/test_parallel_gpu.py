@@ -34,7 +34,7 @@ def _worker(rank, world, port, out_dir, algo_name):
         import paper_2506_00528_b200 as uq
         from paper_2506_00528_b200.parallel import shard_bounds, sharded_search
         torch.cuda.set_device(0)
-        algo = {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "auto": uq.ALGO_AUTO}[algo_name]
+        algo = {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4, "auto": uq.ALGO_AUTO}[algo_name]
         w = datagen.CONFIGS["c2"].scaled(n=150_000, nq=300)
         lo, hi = shard_bounds(w.n, world, rank)
         db = datagen.rows(w, "db", lo, hi - lo, "cuda")
@@ -55,7 +55,7 @@ def _worker(rank, world, port, out_dir, algo_name):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("algo", ["popc", "tc"])
+@pytest.mark.parametrize("algo", ["popc", "tc", "f4"])
 def test_two_rank_sharded_search_real_kernels(tmp_path, algo):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
@@ -67,7 +67,7 @@ def test_two_rank_sharded_search_real_kernels(tmp_path, algo):
     w = datagen.CONFIGS["c2"].scaled(n=150_000, nq=300)
     dbc = uq.encode(datagen.db(w, "cuda"), w.x)
     qc = uq.encode(datagen.queries(w, "cuda"), w.x)
-    algo_c = {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05}[algo]
+    algo_c = {"popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4}[algo]
     s_ref, i_ref = uq.search(qc, dbc, w.d, w.k, algo=algo_c)
     for r in range(2):
         assert np.array_equal(np.load(tmp_path / f"s{r}.npy"), s_ref.cpu().numpy())

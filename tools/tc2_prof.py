@@ -19,21 +19,22 @@ nq = int(sys.argv[3]) if len(sys.argv) > 3 else None
 w = datagen.CONFIGS[cfg].scaled(n=n, nq=nq)
 db = uq.encode(datagen.db(w, "cuda"), w.x)
 q = uq.encode(datagen.queries(w, "cuda"), w.x)
-ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, uq.ALGO_TCGEN05), dtype=torch.uint8, device="cuda")
+ALGO = uq.ALGO_TC_FP4 if os.environ.get("UQ_PROF_ALGO", "f4") == "f4" else uq.ALGO_TCGEN05
+ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, ALGO), dtype=torch.uint8, device="cuda")
 L = uq._L
 L.uq_debug_tc2_prof.argtypes = [ctypes.c_void_p]
 buf = (ctypes.c_ulonglong * 48)()
 for _ in range(2):
-    uq.search(q, db, w.d, w.k, algo=uq.ALGO_TCGEN05, workspace=ws)
+    uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws)
 torch.cuda.synchronize()
 L.uq_debug_tc2_prof(buf)  # reset
 reps = 5
 for _ in range(reps):
-    uq.search(q, db, w.d, w.k, algo=uq.ALGO_TCGEN05, workspace=ws)
+    uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws)
 torch.cuda.synchronize()
 L.uq_debug_tc2_prof(buf)
 c = list(buf)
-out = {"cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
+out = {"algo": os.environ.get("UQ_PROF_ALGO", "f4"), "cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
        "mma_wait_tempty_frac": c[1] / max(c[0], 1), "mma_wait_full_frac": c[2] / max(c[0], 1),
        "prod_wait_empty_frac": c[4] / max(c[3], 1),
        "epi_wait_tfull_frac": c[6] / max(c[5], 1), "epi_filter_frac": c[7] / max(c[5], 1),
