@@ -50,9 +50,7 @@ using namespace ::uq::tc;
 constexpr int BM = 128;               // queries per CTA (pair M = 256)
 constexpr int kProdWarps = 4;         // warps 0-3
 constexpr int kMmaWarp = 3;           // warp 3: also MMA issuer (leader) + TMEM owner
-constexpr int kEpiSets = 2;           // epilogue warp sets, each owns half of a tile's columns
 constexpr int kEpiWarp0 = 4;          // warps 4..11 (warp % 4 = TMEM lane quarter)
-constexpr int kThreads = (kProdWarps + 4 * kEpiSets) * 32;  // 12 warps: 3 per SMSP -> 168 regs
 constexpr uint32_t kTmemCols = 512;   // two accumulators (+ the f4 scale factors)
 constexpr int kOpI8 = 0, kOpF4 = 1;   // operand kind: int8 (kind::i8) / E2M1 (kind::mxf4)
 
@@ -70,7 +68,14 @@ template <int OP> struct Geo {
   static constexpr int MPB = RB / 32;                  // MMAs per block (32 B of K each)
   static constexpr int ACC = BN;                       // TMEM column of the second accumulator
   static constexpr uint32_t SF_COL = 480;              // f4 scale factors: columns [480, 512)
-  static constexpr int CW = BN / kEpiSets;             // accumulator columns per epilogue set
+  // epilogue warp sets (4 warps each, warp % 4 = TMEM lane quarter), each owning
+  // CW columns of a tile: 2 sets = 12 warps = 3 per SMSP -> 168 registers.
+  // f4 histogram mode (seeding; light epilogue, no stream buffers) uses 3 sets
+  // (16 warps, 128 registers) to hide more TMEM-load / vote latency: measured
+  // 155k vs 190k cycles per item on c2; the top-k epilogue spills at 128.
+  static constexpr int sets(int mode) { return (OP == kOpF4 && mode == 1) ? 3 : 2; }
+  static constexpr int threads(int mode) { return (kProdWarps + 4 * sets(mode)) * 32; }
+  static constexpr int cw(int mode) { return BN / sets(mode); }
   static constexpr int bps(int NB) {                   // 128-dim blocks per pipeline stage
     return OP == kOpI8 ? 2 : (NB <= 4 ? NB : (NB + (NB + 3) / 4 - 1) / ((NB + 3) / 4));
   }
@@ -94,9 +99,9 @@ struct Params {
   int64_t n_items;
   int32_t cap;
   int32_t stages;
-  uint32_t* bufs;       // [gridDim.x][kEpiSets*BM][cap]
-  uint64_t* part;       // [s_max*kEpiSets][nq][cap] (top-k mode)
-  int32_t* part_cnt;    // [s_max*kEpiSets][nq] valid entries of each list
+  uint32_t* bufs;       // [gridDim.x][SETS*BM][cap]
+  uint64_t* part;       // [s_max*SETS][nq][cap] (top-k mode)
+  int32_t* part_cnt;    // [s_max*SETS][nq] valid entries of each list
   const int32_t* thr0;  // optional per-query seed D_k (rows with Delta < D_k cannot matter)
   int32_t thr0_stride;
   int64_t row_stride;
@@ -160,11 +165,13 @@ __device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* 
 }
 
 template <int NB, int MODE, int OP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc2_kernel(Params p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MODE), 1) scan_tc2_kernel(Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   using G = Geo<OP>;
   constexpr int BN = G::BN, BH = G::BH;
+  constexpr int kEpiSets = G::sets(MODE);
+  constexpr int kThreads = G::threads(MODE);
   constexpr int kBlkPerStage = G::bps(NB);
   constexpr int kStageBytes = G::stage_bytes(NB);
   constexpr int kAccStride = G::ACC;
@@ -380,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
       const int col = quarter * 32 + lane;    // this thread's query inside the CTA tile
       const int64_t qme = q0 + col;
       const uint32_t tempty_dst = mapa(smem_u32(&tempty[0]), 0);  // leader's tempty[0]
-      constexpr int CW = G::CW;               // columns per set per tile
+      constexpr int CW = G::cw(MODE);         // columns per set per tile
       if (MODE == kModeHist) {
         // Only Delta >= F enters the histogram, F = z nnz(q) / sqrt(d) (z standard
         // deviations of Delta against unrelated codes, z chosen on the host so
@@ -464,15 +471,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) scan_tc
           if (++acc == 2) { acc = 0; aphase ^= 1u; }
           // u16 counters: flush every 128 tiles (128 * 256 rows < 65536 per query)
           if ((tile & 127) == 127) {
-            named_bar_sync(1 + quarter, 64);  // both sets' warps of this quarter
+            named_bar_sync(1 + quarter, 32 * kEpiSets);  // all sets' warps of this quarter
             if (h == 0) hist_flush(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBins : nullptr);
-            named_bar_sync(1 + quarter, 64);
+            named_bar_sync(1 + quarter, 32 * kEpiSets);
           }
         }
-        named_bar_sync(1 + quarter, 64);
+        named_bar_sync(1 + quarter, 32 * kEpiSets);
         const long long tf0 = (p.dbg & 8) ? clk() : 0;
         if (h == 0) hist_flush(s_hist, col, (qme < p.nq && !(p.dbg & 64)) ? p.ghist + (size_t)qme * kHistBins : nullptr);
-        named_bar_sync(1 + quarter, 64);
+        named_bar_sync(1 + quarter, 32 * kEpiSets);
         if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[18], (unsigned long long)(clk() - tf0));
         if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[19], 1ull);
       } else {
@@ -709,7 +716,7 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   pl.ok = true;
   const int npairs = sms / 2;
   pl.n_qtiles = (int32_t)((nq + 2 * tc2::BM - 1) / (2 * tc2::BM));
-  pl.cap = k + 2 * G::CW;
+  pl.cap = k + 2 * G::cw(mode);
   const KeyFmt kf = make_keyfmt(d);
   const int64_t lmax = ((int64_t)kf.rmask + 1) / G::BN * G::BN;
   const int64_t s_min = (n + lmax - 1) / lmax;
@@ -726,13 +733,13 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
     pl.r_hi = (int32_t)hi;
   }
   const int32_t s_max = pl.s_lo + (pl.r_hi > 0 ? 1 : 0);
-  pl.n_chunks = (int64_t)s_max * tc2::kEpiSets;  // lists per query for the merge
+  pl.n_chunks = (int64_t)s_max * G::sets(mode);  // lists per query for the merge
   pl.n_items = QT * pl.s_lo + pl.r_hi;
   const int64_t pairs = pl.n_items < npairs ? pl.n_items : npairs;
   pl.grid = (int32_t)(2 * pairs);
   pl.smem = 1024 + tc2::BM * NB * G::RB + pl.stages * G::stage_bytes(NB) +
             (mode == tc2::kModeHist ? tc2::kHistBytes : 0) + (2 * pl.stages + 4) * 8 + 16;
-  pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * tc2::kEpiSets * tc2::BM * pl.cap * 4;
+  pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * G::sets(mode) * tc2::BM * pl.cap * 4;
   pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * pl.cap * 8;
   return pl;
 }
@@ -751,7 +758,7 @@ static cudaError_t launch_tc2_nb(const tc2::Params& p, const TcPlan& pl, cudaStr
   auto kern = tc2::scan_tc2_kernel<NB, MODE, OP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<pl.grid, tc2::kThreads, pl.smem, st>>>(p);
+  kern<<<pl.grid, tc2::Geo<OP>::threads(MODE), pl.smem, st>>>(p);
   note_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess && getenv("UQ_DEBUG"))
@@ -811,7 +818,7 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st) {
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
-                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
+                (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
                 thr0_stride, row_stride, nullptr, 0, 0.f, tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
@@ -831,7 +838,7 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   float z = inv_norm_cdf(1.0 - ptail);
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
-                (int32_t)(pl.n_chunks / tc2::kEpiSets), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
+                (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
                 nullptr, 0, row_stride, ghist, hs, z, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
