@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of libuq.so (declared and documented in include/uq.h):
 // synchronous argument validation, launch planning, workspace carving.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -29,7 +30,7 @@ static thread_local ScanTimer g_timer;
 
 static void timer_begin(cudaStream_t st, cudaEvent_t* stop, int kind, double evals) {
   *stop = nullptr;
-  if (!g_timer.on) return;
+  if (!g_timer.on || kind < 0) return;   // kind < 0: untimed (the seed fallback pass)
   if (g_timer.used == g_timer.ev.size()) {
     cudaEvent_t a, b;
     if (cudaEventCreate(&a) != cudaSuccess) return;
@@ -119,16 +120,31 @@ struct SeedPlan {
   bool on;
   int64_t rows, stride;
 };
-// Histogram seeding (CTA-pair tensor engine): a cheap epilogue, so a denser
-// sample (1/8) buys a tighter bound.  Top-k seeding (other engines): 1/32.
+// Histogram seeding (CTA-pair tensor engines): a 1/16 sample and an
+// OPTIMISTIC bound -- the largest bin edge with at least need = 3k/16 sampled
+// rows above it, i.e. about 3k rows of the whole database expected above it
+// -- verified after the main scan (a query with fewer than k rows above its
+// bound is searched again without a bound, so results stay exact; with 3x
+// headroom that is a ~5-sigma event).  Top-k seeding (other engines): the
+// exact k-th best of a 1/32 sample.
 static bool hist_seed(uq_algo a, int64_t nq, int32_t d) { return pair_op(a, nq, d) >= 0; }
+// sampled rows that must lie above the histogram seed: need < k is optimistic
+// (verified + fallback), need = k exact.  UQ_SEED_OPT = headroom factor c
+// (default 3; 0 = exact seeds), read per call (tests drive the fallback path).
+static int32_t seed_need(int32_t k, int64_t stride) {
+  const char* e = getenv("UQ_SEED_OPT");
+  const double c = e ? atof(e) : 3.0;
+  if (c <= 0.0) return k;
+  const double need = std::max(8.0, std::ceil(c * (double)k / (double)stride));
+  return need >= (double)k ? k : (int32_t)need;
+}
 static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
   SeedPlan sp{false, 0, 1};
   static const int div_env = [] {
     const char* e = getenv("UQ_SEED_DIV");  // experiment knob: 0 disables seeding
     return e ? atoi(e) : -1;
   }();
-  int seed_div = div_env >= 0 ? div_env : (hist ? 8 : 32);
+  int seed_div = div_env >= 0 ? div_env : (hist ? 16 : 32);
   // large databases: max(2^17, 4096 k) sampled rows already bound D_k tightly
   // (measured on c3 / c5: larger samples only lengthen the seeding scan)
   const int64_t cap = std::max<int64_t>((int64_t)1 << 17, (int64_t)4096 * k);
@@ -144,7 +160,7 @@ static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
 }
 
 struct SearchLayout {
-  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, hist_off, total;
+  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, hist_off, qbase_off, fail_off, total;
 };
 
 static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms,
@@ -160,7 +176,7 @@ static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t 
 }
 
 static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  SearchLayout L{0, 0, 0, 0, 0, 0, 0};
+  SearchLayout L{0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (nq == 0 || n == 0) return L;
   size_t bufs = 0, part = engine_bytes(a, nq, n, d, k, sms, &bufs);
   const bool hist = hist_seed(a, nq, d);
@@ -178,7 +194,9 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   L.seed_s_off = L.cnt_off + cnt_bytes;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
   L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * (hist ? 1 : k) * 4, 256) : 0);
   L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
-  L.total = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 128 * 4, 256) : 0);
+  L.qbase_off = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 128 * 4, 256) : 0);
+  L.fail_off = L.qbase_off + (sp.on && hist ? align_up((size_t)nq * 4, 256) : 0);   // [nq] u32 bin bases
+  L.total = L.fail_off + (sp.on && hist ? align_up((size_t)(nq + 1) * 4, 256) : 0);  // [nq] fail + any
   return L;
 }
 
@@ -191,7 +209,8 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
                                   int32_t d, int32_t k, int64_t id_base, int64_t row_stride,
                                   const int32_t* thr0, int32_t thr0_stride, uint32_t* bufs,
                                   uint64_t* part, int32_t* part_cnt, int32_t* out_s, int64_t* out_id, int sms,
-                                  int timer_kind, cudaStream_t st) {
+                                  int timer_kind, cudaStream_t st, const int32_t* qfail = nullptr,
+                                  const int32_t* any = nullptr) {
   cudaEvent_t ev;
   int64_t lists = 0;
   cudaError_t e;
@@ -199,7 +218,8 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   const int op = pair_op(a, nq, d);
   if (is_tc(a)) {
     const TcPlan tp = plan_tc_for(a, nq, n, d, k, sms);
-    e = op >= 0 ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, op, st)
+    e = op >= 0 ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, op, st,
+                                  qfail, any)
                 : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
     lists = tp.n_chunks;
   } else {
@@ -212,7 +232,8 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   // the pair engine publishes variable-length lists of up to cap entries with counts
   const bool counted = op >= 0;
   const int32_t kin = counted ? plan_tc2(nq, n, d, k, sms, op).cap : k;
-  return launch_merge_keys(part, lists, nq, kin, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr);
+  return launch_merge_keys(part, lists, nq, kin, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr, qfail,
+                           any);
 }
 
 }  // namespace uq
@@ -342,8 +363,8 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   }
   const uq_algo a = resolve_algo(algo, nq, n, d, k, sms);
   if (a == UQ_ALGO_AUTO) return UQ_ERR_UNSUPPORTED;
-  const size_t need = workspace_for(a, nq, n, d, k, sms);
-  if (workspace_bytes < need || (need > 0 && workspace == nullptr)) return UQ_ERR_WORKSPACE;
+  const size_t ws_need = workspace_for(a, nq, n, d, k, sms);
+  if (workspace_bytes < ws_need || (ws_need > 0 && workspace == nullptr)) return UQ_ERR_WORKSPACE;
   if (((uintptr_t)workspace & 255u) != 0) return UQ_ERR_INVALID_ARG;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const SearchLayout L = layout_for(a, nq, n, d, k, sms);
@@ -354,15 +375,17 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   const SeedPlan sp = plan_seed(n, k, hist);
   const int32_t* thr0 = nullptr;
   int32_t thr0_stride = k;
+  const int32_t need = (sp.on && hist) ? seed_need(k, sp.stride) : k;
   if (sp.on && hist) {
-    // Delta histogram of a strided sample -> per-query lower bound on D_k
+    // Delta histogram of a strided sample -> per-query bound on D_k
     int32_t* thr = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
     uint32_t* ghist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
+    uint32_t* qbase = reinterpret_cast<uint32_t*>(ws + L.qbase_off);
     if (cudaMemsetAsync(ghist, 0, (size_t)nq * 128 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)sp.rows);
-    cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, sp.stride, ghist, thr, sms,
-                                         pair_op(a, nq, d), st);
+    cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, need, sp.stride, ghist, qbase, thr,
+                                         sms, pair_op(a, nq, d), st);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = thr;
@@ -378,6 +401,17 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
   cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, thr0_stride, bufs, part,
                                  part_cnt, out_scores, out_ids, sms, 0, st);
+  if (e != cudaSuccess || !(sp.on && hist && need < k)) return from_cuda(e);
+  // optimistic seeds: queries with fewer than k rows above their bound are
+  // searched again without one (device-side flags: no host round trip; the
+  // fallback scan and merge are no-ops when nothing failed)
+  int32_t* fail = reinterpret_cast<int32_t*>(ws + L.fail_off);
+  int32_t* any = fail + nq;
+  if (cudaMemsetAsync(any, 0, 4, st) != cudaSuccess) return UQ_ERR_CUDA;
+  e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
+  if (e != cudaSuccess) return UQ_ERR_CUDA;
+  e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, nullptr, 0, bufs, part, part_cnt, out_scores,
+                     out_ids, sms, -1, st, fail, any);
   return from_cuda(e);
 }
 

@@ -22,7 +22,8 @@ cudaError_t launch_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsig
                                int sms, cudaStream_t st);
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
                               int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
-                              const int32_t* counts = nullptr);
+                              const int32_t* counts = nullptr, const int32_t* only = nullptr,
+                              const int32_t* any = nullptr);
 cudaError_t launch_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, const void* db, int64_t n,
                           int64_t ld, int32_t d, const int64_t* cand, int32_t n_cand, int32_t k, float* out_cos,
                           int64_t* out_ids, cudaStream_t st);
@@ -61,12 +62,23 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
 TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op);
 cudaError_t tc2_prof_read(unsigned long long* out48);
 TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op);
+// Seeding: histogram scan over rows {i * row_stride : i < n}, then per query
+// thr[q] = the largest bin edge with at least `need` sampled rows at or above
+// it (INT32_MIN if none).  need = k: an exact lower bound on D_k; need < k: an
+// optimistic bound, checked after the main scan by launch_seed_verify.
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
-                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms, int op,
-                                 cudaStream_t st);
+                                 int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
+                                 int32_t* thr, int sms, int op, cudaStream_t st);
+// After a search with optimistic seeds: fail[q] = 1 iff q was filtered
+// (thr[q] != INT32_MIN) and fewer than k rows passed (its k-th result is
+// padding); *any |= 1 if some query failed (*any must be zero on entry).
+cudaError_t launch_seed_verify(const int64_t* out_ids, int64_t nq, int32_t k, const int32_t* thr, int32_t* fail,
+                               int32_t* any, cudaStream_t st);
+// qfail / any_fail (optional, the seed fallback pass): the launch is a no-op
+// unless *any_fail, and only pair tiles holding a query with qfail[q] run.
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
-                            cudaStream_t st);
+                            cudaStream_t st, const int32_t* qfail = nullptr, const int32_t* any_fail = nullptr);
 
 }  // namespace uq

@@ -34,6 +34,8 @@ struct MergeParams {
   int64_t* out_id;
   int32_t stage_cap;  // candidates staged in shared memory if C <= stage_cap
   const int32_t* counts;  // source (a), optional: valid entries per list [lists][nq] (rest unread, empty)
+  const int32_t* only;    // optional: merge only queries q with only[q] != 0 (seed fallback pass)
+  const int32_t* any;     // optional: the whole launch is a no-op unless *any != 0
 };
 
 template <bool FROM_SI>
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   __shared__ int s_b, s_above, s_inb;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = blockIdx.x;
+  if ((p.any != nullptr && *p.any == 0) || (p.only != nullptr && p.only[q] == 0)) return;
   __shared__ int s_off[kMergeMaxLists + 1];
   int64_t C = p.lists * p.kin;
   const int P = 1 << bitlen((unsigned)(p.k - 1 > 0 ? p.k - 1 : 1));  // pow2 >= k (>= 2)
@@ -222,14 +225,14 @@ static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t
 
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
                               int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
-                              const int32_t* counts) {
-  MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0, counts};
+                              const int32_t* counts, const int32_t* only, const int32_t* any) {
+  MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0, counts, only, any};
   return launch_merge_common(p, false, st);
 }
 
 cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
                             int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
-  MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0, nullptr};
+  MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0, nullptr, nullptr, nullptr};
   return launch_merge_common(p, true, st);
 }
 

@@ -20,10 +20,11 @@
 //   kTopK  per-query top-k streams (threshold filter in registers, append to
 //          a per-stream buffer, warp-cooperative cut back to k), lists of
 //          64-bit global keys per (chunk, column half) for the merge kernel;
-//   kHist  threshold seeding: per-query histogram of Delta >= F in bins of
-//          2^hshift (shared-memory atomics, flushed to a global [nq][128]
-//          histogram; F ~ 2 sigma of unrelated-code Delta filters ~98% first).  At least sum_{b' >= b} hist[b'] rows have Delta >=
-//          b << hshift, so thr_from_hist_kernel's per-query bound is exact.
+//   kHist  threshold seeding: per-query histogram of Delta >= F_q in 128 bins
+//          of width 2^hs_q spanning [F_q, nnz(q)] (shared-memory atomics,
+//          flushed to a global [nq][128] histogram; F_q ~ 2-3 sigma of
+//          unrelated-code Delta filters most scores first).  At least
+//          sum_{b' >= b} hist[b'] sampled rows have Delta >= F_q + (b << hs_q).
 //
 // Warps: 0-3 producers (one thread per DB row of this CTA's 128-row half; the
 // int8 expansion is bound by the integer ALU pipe of each SM sub-partition, so
@@ -106,8 +107,10 @@ struct Params {
   int32_t thr0_stride;
   int64_t row_stride;
   uint32_t* ghist;      // kHist: [nq][kHistBins]
-  int32_t hshift;       // kHist: bin = Delta >> hshift
-  float zfloor;         // kHist: only Delta >= zfloor * nnz(q) / sqrt(d) is counted
+  float zfloor;         // kHist: only Delta >= F = zfloor * nnz(q) / sqrt(d) is counted
+  uint32_t* qbase;      // kHist: per query (hs << 16) | F, bin = (Delta - F) >> hs
+  const int32_t* qfail; // top-k, optional (seed fallback pass): run only pair tiles with a failed query
+  const int32_t* any_fail;  // optional: the launch is a no-op unless *any_fail
   int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads,
                         // 8 cycle accounting, 16 no producer proxy fence
 };
@@ -194,6 +197,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
   uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps per set
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  // seed fallback pass with nothing to redo: every thread of both CTAs leaves
+  if (p.any_fail != nullptr && *p.any_fail == 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t_entry = PROF_ON ? clk() : 0;
   const uint32_t cr = cluster_ctarank();
@@ -243,6 +248,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
     const int64_t rows = it.rows;
     const int ntiles = (int)((rows + BN - 1) / BN);
 
+    if (p.qfail != nullptr) {
+      // fallback pass: skip pair tiles without a failed query (both CTAs test
+      // the same 256 queries, so both skip or both run)
+      int f = 0;
+      for (int i = threadIdx.x; i < 2 * BM; i += kThreads) {
+        const int64_t qq = (int64_t)it.t * (2 * BM) + i;
+        if (qq < p.nq && p.qfail[qq] != 0) f = 1;
+      }
+      if (!__syncthreads_or(f)) continue;
+    }
     // ---- A: this CTA's 128 query codes, expanded (all threads) ----
     cluster_sync();  // previous item retired in both CTAs (A is read by the pair's MMAs)
     for (int u = threadIdx.x; u < BM * NB; u += kThreads) {
@@ -394,9 +409,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         // that ~4k unrelated sample rows still clear it): the count above any
         // bin edge stays a lower bound, and almost every score costs one compare.
         int floor_m1 = 0x7fffffff;
+        int nnz = 0;
         if (qme < p.nq) {
           const uint8_t* qc = p.q + qme * cb;
-          int nnz = 0;
           for (int b = 0; b < NB; ++b) {
             const uint4 a = *reinterpret_cast<const uint4*>(qc + b * 16);
             const uint4 c = *reinterpret_cast<const uint4*>(qc + pb + b * 16);
@@ -404,6 +419,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                    __popc(c.z) + __popc(c.w);
           }
           floor_m1 = max(0, (int)(p.zfloor * (float)nnz * rsqrtf((float)p.d))) - 1;
+        }
+        // bins of width 2^hs_q from F = floor_m1 + 1 up to nnz(q) >= any Delta
+        int hs_q = 0;
+        if (qme < p.nq) {
+          const int range = max(nnz - floor_m1, 1);   // Delta in [F, nnz]: range values
+          hs_q = range > kHistBins ? 32 - __clz(range - 1) - 7 : 0;
+          if (h == 0) p.qbase[qme] = ((uint32_t)hs_q << 16) | (uint32_t)(floor_m1 + 1);
         }
         const bool raw = OP == kOpF4 && __all_sync(kFull, floor_m1 >= 0);
         const int fl = OP != kOpF4 ? floor_m1 : raw ? __float_as_int((float)floor_m1) : min(floor_m1, 4096) + kF4Bias;
@@ -457,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                     const int sc = (int)v[4 * i + j];
                     if (sc > fl) {
                       const int dv = OP != kOpF4 ? sc : raw ? __float2int_rn(__int_as_float(sc)) : sc - kF4Bias;
-                      const uint32_t b = min((uint32_t)dv >> p.hshift, (uint32_t)(kHistBins - 1));
+                      const uint32_t b = min((uint32_t)(dv - floor_m1 - 1) >> hs_q, (uint32_t)(kHistBins - 1));
                       atomicAdd(s_hist + (b >> 1) * BM + col, (b & 1u) ? 0x10000u : 1u);
                     }
                   }
@@ -651,10 +673,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
   if (threadIdx.x == 0) PROF_ADD(14, 1);
 }
 
-// kHist -> per-query seed: thr[q] = (largest b with sum_{b' >= b} hist[q][b'] >= k) << hshift,
-// INT32_MIN if fewer than k sampled rows were counted.  One warp per query
-// (lane l: bins 4l .. 4l+3); clears the histogram.
-__global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, int32_t hshift, int32_t* thr) {
+// kHist -> per-query seed: thr[q] = F_q + (b << hs_q) for the largest bin b with
+// sum_{b' >= b} hist[q][b'] >= need (at least `need` sampled rows have Delta >=
+// that edge), INT32_MIN if fewer than need sampled rows were counted.  One warp
+// per query (lane l: bins 4l .. 4l+3); clears the histogram.
+__global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, const uint32_t* qbase, int32_t* thr) {
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (q >= nq) return;
@@ -678,8 +701,20 @@ __global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, int
   const int L = 31 - __clz(ok);
   if (lane == L) {
     const int j = (s3 >= (uint32_t)k) ? 3 : (s2 >= (uint32_t)k) ? 2 : (s1 >= (uint32_t)k) ? 1 : 0;
-    thr[q] = (4 * L + j) << hshift;
+    const uint32_t qb = qbase[q];
+    thr[q] = (int32_t)(qb & 0xffffu) + ((4 * L + j) << (qb >> 16));
   }
+}
+
+// fail[q] = the query was filtered by a seed and its k-th result is padding
+// (fewer than k rows passed the optimistic bound): it must be searched again
+__global__ void seed_verify_kernel(const int64_t* out_ids, int64_t nq, int32_t k, const int32_t* thr, int32_t* fail,
+                                   int32_t* any) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const bool f = thr[q] != INT32_MIN && out_ids[q * k + (k - 1)] < 0;
+  fail[q] = f ? 1 : 0;
+  if (f) atomicOr(any, 1);
 }
 
 }  // namespace tc2
@@ -697,10 +732,6 @@ static int tc2_stages(int NB, int mode) {
 }
 static int tc2_max_nb(int op) { return op == tc2::kOpF4 ? 12 : 8; }
 
-static int tc2_hist_shift(int32_t d) {
-  int hs = bitlen((uint32_t)d) - 7;  // (d >> hs) < 128
-  return hs < 0 ? 0 : hs;
-}
 
 // Pairs: the query set is cut into 256-query pair tiles; each of the SMs/2
 // pairs gets one (pair tile, DB chunk) item when the tiles do not cover them.
@@ -816,10 +847,10 @@ cudaError_t tc2_prof_read(unsigned long long* out48) {
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
-                            cudaStream_t st) {
+                            cudaStream_t st, const int32_t* qfail, const int32_t* any_fail) {
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
-                thr0_stride, row_stride, nullptr, 0, 0.f, tc2_dbg()};
+                thr0_stride, row_stride, nullptr, 0.f, nullptr, qfail, any_fail, tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
 
@@ -827,11 +858,10 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
 // thr[q] (stride 1) from the histogram.  ghist: [nq][128] u32, zero on entry
 // (left zero on exit).
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
-                                 int32_t k, int64_t row_stride, uint32_t* ghist, int32_t* thr, int sms, int op,
-                                 cudaStream_t st) {
+                                 int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
+                                 int32_t* thr, int sms, int op, cudaStream_t st) {
   const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;
-  const int hs = tc2_hist_shift(d);
   // floor: about 4k of n unrelated rows exceed it (Gaussian tail), z in [0, 4]
   double ptail = 4.0 * (double)k / (double)(n > 0 ? n : 1);
   if (ptail > 0.5) ptail = 0.5;
@@ -839,10 +869,17 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
-                nullptr, 0, row_stride, ghist, hs, z, tc2_dbg()};
+                nullptr, 0, row_stride, ghist, z, qbase, nullptr, nullptr, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
-  tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, k, hs, thr);
+  tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, need, qbase, thr);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed_verify(const int64_t* out_ids, int64_t nq, int32_t k, const int32_t* thr, int32_t* fail,
+                               int32_t* any, cudaStream_t st) {
+  tc2::seed_verify_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(out_ids, nq, k, thr, fail, any);
   note_launch();
   return cudaGetLastError();
 }

@@ -311,3 +311,16 @@ def test_errors_are_loud(uq):
         uq.encode(torch.zeros(4, 16, device="cuda"), 0)
     with pytest.raises(ValueError):
         uq.encode(torch.zeros(4, 16), 4)          # CPU tensor: no CPU path
+
+
+@pytest.mark.parametrize("algo", ["tc", "f4"])
+@pytest.mark.parametrize("opt,k", [("0", 100), ("3", 100), ("0.01", 500), ("0.01", 100)])
+@pytest.mark.parametrize("mode", ["normal", "dup"])
+def test_seed_optimistic_fallback(uq, orc, monkeypatch, algo, opt, k, mode):
+    """Pair engines seed with an OPTIMISTIC bound (about c*k rows expected above
+    it, c = UQ_SEED_OPT, default 3; 0 = exact bound).  A query with fewer than k
+    rows above its bound is searched again without one; c = 0.01 forces that
+    fallback (need = 8 sampled rows, ~128 expected above < k = 500).  Results
+    stay bit-exact in every case."""
+    monkeypatch.setenv("UQ_SEED_OPT", opt)
+    _search_case(uq, orc, algo, 256, 128, 131072, 300, k, seed=5 + k, mode=mode)
