@@ -121,23 +121,31 @@ struct SeedPlan {
   int64_t rows, stride;
 };
 // Histogram seeding (CTA-pair tensor engines): a 1/16 sample and an
-// OPTIMISTIC bound -- the largest bin edge with at least need = 3k/16 sampled
-// rows above it, i.e. about 3k rows of the whole database expected above it
-// -- verified after the main scan (a query with fewer than k rows above its
-// bound is searched again without a bound, so results stay exact; with 3x
-// headroom that is a ~5-sigma event).  Top-k seeding (other engines): the
+// OPTIMISTIC bound -- the largest bin edge with at least `need` sampled rows
+// above it (seed_need: a few times k rows of the whole database expected
+// above it) -- verified after the main scan: a query with fewer than k rows
+// above its bound is searched again without a bound, so results stay exact.  Top-k seeding (other engines): the
 // exact k-th best of a 1/32 sample.
 static bool hist_seed(uq_algo a, int64_t nq, int32_t d) { return pair_op(a, nq, d) >= 0; }
 // sampled rows that must lie above the histogram seed: need < k is optimistic
-// (verified + fallback), need = k exact.  UQ_SEED_OPT = headroom factor c
-// (default 3; 0 = exact seeds), read per call (tests drive the fallback path).
+// (verified + fallback), need = k exact.  With 1/stride sampling a bound with
+// fewer than k rows above it has about lambda = k / stride sampled rows above
+// (Poisson), so need = lambda + 5.5 sqrt(lambda) + 2 (at least 8) makes a
+// fallback a > 5-sigma event per query (c2: 22 of 62500 sampled rows, about
+// 350 rows expected above).  UQ_SEED_OPT = c overrides with need = c k / stride
+// (0: exact seeds); read per call, the tests drive the fallback path with it.
 static int32_t seed_need(int32_t k, int64_t stride) {
-  const char* e = getenv("UQ_SEED_OPT");
-  const double c = e ? atof(e) : 3.0;
-  if (c <= 0.0) return k;
-  const double need = std::max(8.0, std::ceil(c * (double)k / (double)stride));
+  const double lam = (double)k / (double)stride;
+  double need = std::ceil(lam + 5.5 * std::sqrt(lam) + 2.0);
+  if (const char* e = getenv("UQ_SEED_OPT")) {
+    const double c = atof(e);
+    if (c <= 0.0) return k;
+    need = std::ceil(c * lam);
+  }
+  need = std::max(8.0, need);
   return need >= (double)k ? k : (int32_t)need;
 }
+
 static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
   SeedPlan sp{false, 0, 1};
   static const int div_env = [] {
