@@ -456,17 +456,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
               // 120-column sets end on a group boundary), element-wise only in a
               // database's partial last group
               const int rem = ncols - c0;
+              if (rem & 3) {   // rare: a database's partial last group
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (4 * i >= rem) {
-                  cm[i] = (int)pad;
-                } else if (4 * i + 4 > rem) {
+                for (int j = 0; j < 32; ++j)
+                  if (j >= rem) v[j] = pad;
 #pragma unroll
-                  for (int j = 0; j < 4; ++j)
-                    if (4 * i + j >= rem) v[4 * i + j] = pad;
+                for (int i = 0; i < 8; ++i)
                   cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
-                }
               }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) cm[i] = 4 * i >= rem ? (int)pad : cm[i];   // selects, no branches
             }
             const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                         max(cm[6], cm[7]));
@@ -550,17 +549,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
               // 120-column sets end on a group boundary), element-wise only in a
               // database's partial last group
               const int rem = ncols - c0;
+              if (rem & 3) {   // rare: a database's partial last group
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (4 * i >= rem) {
-                  cm[i] = (int)pad;
-                } else if (4 * i + 4 > rem) {
+                for (int j = 0; j < 32; ++j)
+                  if (j >= rem) v[j] = pad;
 #pragma unroll
-                  for (int j = 0; j < 4; ++j)
-                    if (4 * i + j >= rem) v[4 * i + j] = pad;
+                for (int i = 0; i < 8; ++i)
                   cm[i] = max(__vimax3_s32((int)v[4 * i], (int)v[4 * i + 1], (int)v[4 * i + 2]), (int)v[4 * i + 3]);
-                }
               }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) cm[i] = 4 * i >= rem ? (int)pad : cm[i];   // selects, no branches
             }
             const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                         max(cm[6], cm[7]));
