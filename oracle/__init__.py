@@ -63,6 +63,10 @@ def lib():
         L.orc_check_codes.argtypes = [vp, i64, i32]
         L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_rerank.argtypes = [vp, i64, vp, i64, i32, vp, i32, i32, vp, vp]
+        L.orc_quantize_i8.argtypes = [vp, i64, i32, vp]
+        L.orc_quantize_i8.restype = None
+        L.orc_knn_asym.argtypes = [vp, i64, vp, i64, i32, i32, i64, vp, vp]
+        L.orc_knn_asym.restype = None
         L.orc_rerank.restype = None
         L.orc_set_threads.restype = ctypes.c_int
         L.orc_check_codes.restype = i64
@@ -154,6 +158,34 @@ def knn(qcodes, dbcodes, d: int, k: int, id_base: int = 0):
     s = np.zeros((nq, k), dtype=np.int32)
     ids = np.zeros((nq, k), dtype=np.int64)
     lib().orc_knn(_p(qc), nq, _p(dc), n, d, k, id_base, _p(s), _p(ids))
+    return s, ids
+
+
+def quantize_i8(u) -> np.ndarray:
+    """Query quantisation to int8 (R15): per row, fp32 scale 127/max|u|,
+    round half to even, fp32 arithmetic.  f16 / bf16 inputs widen exactly to f32."""
+    u = np.asarray(u)
+    if u.dtype not in (np.float16, np.float32):
+        raise TypeError("quantize_i8 takes f16 / f32 rows (widened exactly to f32)")
+    u32 = np.ascontiguousarray(u.astype(np.float32))
+    if u32.ndim == 1:
+        u32 = u32[None, :]
+    n, d = u32.shape
+    out = np.zeros((n, d), dtype=np.int8)
+    lib().orc_quantize_i8(_p(u32), n, d, _p(out))
+    return out
+
+
+def knn_asym(q8, dbcodes, d: int, k: int, id_base: int = 0):
+    """Single-operand kNN: int8 query x packed ternary rows by masked
+    addition; (scores[nq][k] int32, ids[nq][k] int64), (score desc, id asc)."""
+    q = np.ascontiguousarray(q8, dtype=np.int8)
+    dc = np.ascontiguousarray(dbcodes, dtype=np.uint8)
+    nq, n = q.shape[0], dc.shape[0]
+    assert q.shape[1] == d
+    s = np.zeros((nq, k), dtype=np.int32)
+    ids = np.zeros((nq, k), dtype=np.int64)
+    lib().orc_knn_asym(_p(q), nq, _p(dc), n, d, k, id_base, _p(s), _p(ids))
     return s, ids
 
 

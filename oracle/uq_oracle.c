@@ -175,6 +175,66 @@ void orc_knn(const uint8_t* qc, int64_t nq, const uint8_t* dc, int64_t n, int32_
 }
 
 /* ------------------------------------------------------------------------ */
+/* Single-operand translation (Sec. 6.1): only the database is      */
+/* ternary; the query stays in the original space "quantised to 8-bit         */
+/* integers", and the scalar product is the masked addition of P:379          */
+/* (Sec. 5.1.2): add q_i where v_i^+ = 1, subtract q_i where v_i^- = 1.        */
+/* Quantisation (R15; the paper names no scheme): per vector, scale =         */
+/* 127 / max_i |u_i| and q_i = round-half-even(u_i * scale), both in fp32      */
+/* arithmetic; an all-zero vector maps to zeros.                               */
+/* ------------------------------------------------------------------------ */
+void orc_quantize_i8(const float* u, int64_t n, int32_t d, int8_t* out) {
+  for (int64_t r = 0; r < n; ++r) {
+    const float* row = u + r * d;
+    float m = 0.0f;
+    for (int32_t i = 0; i < d; ++i) {
+      const float a = fabsf(row[i]);
+      if (a > m) m = a;
+    }
+    const float scale = (m > 0.0f) ? 127.0f / m : 0.0f;
+    for (int32_t i = 0; i < d; ++i) {
+      float q = rintf(row[i] * scale);
+      if (q > 127.0f) q = 127.0f;
+      if (q < -127.0f) q = -127.0f;
+      out[r * d + i] = (int8_t)q;
+    }
+  }
+}
+
+/* masked addition of one int8 query against one packed ternary row */
+static int32_t masked_add(const int8_t* q, const uint8_t* code, int32_t d) {
+  const int64_t pb = orc_plane_bytes(d);
+  int32_t s = 0;
+  for (int32_t i = 0; i < d; ++i) {
+    const int pos = (code[i / 8] >> (i % 8)) & 1;
+    const int neg = (code[pb + i / 8] >> (i % 8)) & 1;
+    if (pos) s += q[i];
+    if (neg) s -= q[i];
+  }
+  return s;
+}
+
+/* Exhaustive kNN by masked addition: order (score desc, id asc), keep k, pad. */
+void orc_knn_asym(const int8_t* q8, int64_t nq, const uint8_t* dc, int64_t n, int32_t d, int32_t k,
+                  int64_t id_base, int32_t* out_s, int64_t* out_id) {
+  const int64_t cb = orc_code_bytes(d);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < nq; ++q) {
+    orc_cand_t* c = (orc_cand_t*)malloc(sizeof(orc_cand_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t r = 0; r < n; ++r) {
+      c[r].s = masked_add(q8 + q * d, dc + r * cb, d);
+      c[r].id = id_base + r;
+    }
+    qsort(c, (size_t)n, sizeof(orc_cand_t), cmp_cand);
+    for (int32_t j = 0; j < k; ++j) {
+      out_s[q * k + j] = (j < n) ? c[j].s : INT32_MIN;
+      out_id[q * k + j] = (j < n) ? c[j].id : -1;
+    }
+    free(c);
+  }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Cosine ground truth in fp64 (Sec. 1.1; R12): normalise each row,  */
 /* cos = <q^, u^>; order by (cos desc, id asc); keep k.                        */
 /* ------------------------------------------------------------------------ */

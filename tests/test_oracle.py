@@ -320,3 +320,50 @@ def test_rerank(orc):
     s3, i3 = orc.rerank(q, db, bad, 4)
     assert (i3[:, 2:] == -1).all() and np.isinf(s3[:, 2:]).all()
     assert all(set(i3[r, :2].tolist()) == {3, 7} for r in range(6))
+
+
+def test_quantize_i8_closed_forms(orc):
+    """R15 (P:507-509 names no scheme): per-vector scale 127/max|u| in fp32, round
+    half to even.  Closed forms, the half-way ties, and exact invariances."""
+    e = np.zeros((1, 9), np.float32)
+    e[0, 4] = 3.7
+    q = orc.quantize_i8(e)
+    assert q[0, 4] == 127 and np.count_nonzero(q) == 1
+    # 127 * 0.5 = 63.5 -> 64 (even), 127 * 0.25 = 31.75 -> 32, -63.5 -> -64
+    q = orc.quantize_i8(np.array([[1.0, -1.0, 0.5, 0.25, -0.5, 0.0]], np.float32))
+    assert q.tolist() == [[127, -127, 64, 32, -64, 0]]
+    # 127/3 * 1.5 = 63.5 exactly?  not in fp32 -- check against an explicit fp32 recomputation
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((50, 37)).astype(np.float32)
+    q = orc.quantize_i8(u)
+    m = np.abs(u).max(axis=1, keepdims=True)
+    scale = (np.float32(127.0) / m).astype(np.float32)
+    ref = np.clip(np.rint((u * scale).astype(np.float32)), -127, 127).astype(np.int8)
+    assert np.array_equal(q, ref)
+    assert np.array_equal(orc.quantize_i8(-u), -q)                  # symmetric rounding
+    assert np.array_equal(orc.quantize_i8(u * np.float32(8.0)), q)  # 2^k scaling is exact
+    assert np.array_equal(orc.quantize_i8(np.zeros((2, 5), np.float32)), np.zeros((2, 5), np.int8))
+    assert (np.abs(q).max(axis=1) == 127).all()
+
+
+def test_knn_asym_masked_addition(orc):
+    """Single-operand search by masked addition: (1) with a
+    ternary query as the int8 operand it equals the paper's b2sp kNN exactly
+    (Table 3 pins b2sp); (2) its scores equal an exact integer matmul with the
+    unpacked codes; (3) its ranking equals a lexsort brute force."""
+    rng = np.random.default_rng(12)
+    d, n, nq, k = 200, 400, 7, 25
+    u = rng.standard_normal((n + nq, d)).astype(np.float32)
+    codes = orc.pack(orc.encode(u[:n], 67))
+    qv = orc.encode(u[n:], 67)
+    s_sym, i_sym = orc.knn(orc.pack(qv), codes, d, k, id_base=3)
+    s_asym, i_asym = orc.knn_asym(qv.astype(np.int8), codes, d, k, id_base=3)
+    assert np.array_equal(s_sym, s_asym) and np.array_equal(i_sym, i_asym)
+    q8 = orc.quantize_i8(u[n:])
+    s, ids = orc.knn_asym(q8, codes, d, n)
+    full = q8.astype(np.int64) @ orc.unpack(codes, d).astype(np.int64).T
+    for r in range(nq):
+        order = np.lexsort((np.arange(n), -full[r]))
+        assert np.array_equal(ids[r], order) and np.array_equal(s[r], full[r][order])
+    s2, i2 = orc.knn_asym(q8, codes[:5], d, 8)   # n < k: padding
+    assert (i2[:, 5:] == -1).all() and (s2[:, 5:] == np.iinfo(np.int32).min).all()
