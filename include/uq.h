@@ -149,6 +149,37 @@ uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d,
                          unsigned long long* bad_rows, uq_stream_t stream);
 
 /*
+ * uq_quantize_i8 -- query quantisation for single-operand search (P:507-509:
+ * queries "quantised to 8-bit integers"; the scheme is reading R15 of
+ * DESIGN.md): per row, scale = 127 / max_i |u_i| and out_i =
+ * round-half-even(u_i * scale) in IEEE fp32, clamped to [-127, 127]; an
+ * all-zero row maps to zeros.
+ *   u   [n][ld] f32 / f16 / bf16 (element type dt), ld >= d
+ *   out [n][ldo] int8, ldo >= d; columns >= d are not written.
+ * Errors: UQ_ERR_INVALID_ARG for bad sizes / null pointers / misalignment,
+ * UQ_ERR_UNSUPPORTED for d > UQ_MAX_D.
+ */
+uq_status uq_quantize_i8(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld, int8_t* out,
+                         int64_t ldo, uq_stream_t stream);
+
+/*
+ * uq_search_asym -- single-operand exhaustive kNN (Sec. 6.1): only
+ * the database is ternary; each query is an int8 vector q (e.g. from
+ * uq_quantize_i8) and the score of row v is the masked addition of P:379,
+ * S = sum_{v_i = +1} q_i - sum_{v_i = -1} q_i (an exact int32, |S| <= 127 d).
+ * Results as uq_search: (S desc, id asc), ids = id_base + row, padding
+ * (INT32_MIN, -1).
+ *   q8 [nq][ldq] int8 (device), ldq >= d; dbcodes [n][code_bytes(d)] (16-B
+ *   aligned); workspace >= uq_search_asym_workspace() bytes, 256-B aligned.
+ * Runs on the int8 tcgen05 CTA-pair engine (the queries are the A operand):
+ * d <= 1024, otherwise UQ_ERR_UNSUPPORTED.  Other errors as uq_search.
+ */
+uq_status uq_search_asym_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes);
+uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, int64_t n,
+                         int32_t d, int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
+                         void* workspace, size_t workspace_bytes, uq_stream_t stream);
+
+/*
  * uq_rerank -- k@n: re-rank proxy-space candidates in the original space
  * (Sec. 5.3: "n > k results are found from the approximate search,
  * which are then reordered with respect to the original space, with the best k

@@ -18,6 +18,7 @@ __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
     "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05", "ALGO_TC_FP4",
     "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex", "rerank",
+    "quantize_i8", "search_asym", "search_asym_workspace",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -52,13 +53,16 @@ def _load():
     L.uq_merge_topk.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
     L.uq_rerank.argtypes = [vp, i32, i64, i64, vp, i64, i64, i32, vp, i32, i32, vp, vp, vp]
     L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
+    L.uq_quantize_i8.argtypes = [vp, i32, i64, i32, i64, vp, i64, vp]
+    L.uq_search_asym_workspace.argtypes = [i64, i64, i32, i32, ctypes.POINTER(sz)]
+    L.uq_search_asym.argtypes = [vp, i64, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
     L.uq_timing_enable.argtypes = [i32]
     L.uq_timing_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
     L.uq_timing_collect_ex.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
                                        ctypes.POINTER(ctypes.c_double)]
     for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_timing_collect_ex", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
-              "uq_check_codes", "uq_rerank"):
+              "uq_check_codes", "uq_rerank", "uq_quantize_i8", "uq_search_asym_workspace", "uq_search_asym"):
         getattr(L, f).restype = i32
     return L
 
@@ -186,6 +190,49 @@ def search(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base:
     _check("uq_search", _L.uq_search_ex(_ptr(qcodes), nq, _ptr(dbcodes), n, d, k, id_base,
                                         _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
                                         workspace.numel(), algo, _stream(stream)))
+    return out
+
+
+def quantize_i8(u: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """int8 queries for single-operand search (uq_quantize_i8, R15): per row
+    round-half-even(u * 127 / max|u|) in fp32 -> [n][d] int8."""
+    _dev(u, "u")
+    if u.dim() != 2 or u.stride(1) != 1 or u.dtype not in _DT:
+        raise ValueError("u must be 2-D f32/f16/bf16 with unit column stride")
+    n, d = u.shape
+    if out is None:
+        out = torch.empty((n, d), dtype=torch.int8, device=u.device)
+    _check("uq_quantize_i8", _L.uq_quantize_i8(_ptr(u), _DT[u.dtype], n, d, u.stride(0), _ptr(out),
+                                               out.stride(0), _stream(stream)))
+    return out
+
+
+def search_asym_workspace(nq: int, n: int, d: int, k: int) -> int:
+    b = ctypes.c_size_t(0)
+    _check("uq_search_asym_workspace", _L.uq_search_asym_workspace(nq, n, d, k, ctypes.byref(b)))
+    return int(b.value)
+
+
+def search_asym(q8: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base: int = 0,
+                workspace: Optional[torch.Tensor] = None,
+                out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
+                stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Single-operand kNN (uq_search_asym): int8 queries q8 [nq][d]
+    against ternary codes by masked addition; (scores int32, ids int64) [nq][k]."""
+    _dev(q8, "q8"); _dev(dbcodes, "dbcodes")
+    if q8.dtype != torch.int8 or q8.dim() != 2 or q8.stride(1) != 1:
+        raise ValueError("q8 must be a 2-D int8 tensor with unit column stride")
+    nq, n = q8.shape[0], dbcodes.shape[0]
+    dev = q8.device
+    if out is None:
+        out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
+               torch.empty((nq, k), dtype=torch.int64, device=dev))
+    need = search_asym_workspace(nq, n, d, k)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    _check("uq_search_asym", _L.uq_search_asym(_ptr(q8), nq, q8.stride(0), _ptr(dbcodes), n, d, k, id_base,
+                                               _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
+                                               workspace.numel(), _stream(stream)))
     return out
 
 

@@ -456,6 +456,112 @@ uq_status uq_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, const v
                                  (cudaStream_t)stream));
 }
 
+uq_status uq_quantize_i8(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld, int8_t* out, int64_t ldo,
+                         uq_stream_t stream) {
+  g_launches = 0;
+  if (n < 0 || d < 1 || ld < d || ldo < d) return UQ_ERR_INVALID_ARG;
+  if (dt != UQ_F32 && dt != UQ_F16 && dt != UQ_BF16) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D) return UQ_ERR_UNSUPPORTED;
+  if (n == 0) return UQ_OK;
+  if (!u || !out) return UQ_ERR_INVALID_ARG;
+  const size_t es = (dt == UQ_F32) ? 4 : 2;
+  if (((uintptr_t)u % es) != 0) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_quantize_i8(u, dt, n, d, ld, out, ldo, (cudaStream_t)stream));
+}
+
+// ---- single-operand search: int8 queries x ternary database ----
+// Runs on the int8 CTA-pair engine with the queries as the A operand; scores
+// |S| <= 127 d set the key format.  Seeding: the exact k-th best of a 1/32
+// sample (a top-k scan of the sample + merge), as for the other engines.
+struct AsymLayout {
+  bool ok;
+  TcPlan main, seed;
+  SeedPlan sp;
+  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, total;
+};
+static AsymLayout asym_layout(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
+  AsymLayout L{};
+  L.main = plan_tc2(nq, n, d, k, sms, 0, 127 * d);
+  L.ok = L.main.ok;
+  if (!L.ok) return L;
+  L.sp = plan_seed(n, k, false);
+  size_t bufs = align_up(L.main.buf_bytes, 256), part = align_up(L.main.part_bytes, 256);
+  int64_t chunks = L.main.n_chunks;
+  if (L.sp.on) {
+    L.seed = plan_tc2(nq, L.sp.rows, d, k, sms, 0, 127 * d);
+    if (!L.seed.ok) { L.sp.on = false; }
+    else {
+      bufs = std::max(bufs, align_up(L.seed.buf_bytes, 256));
+      part = std::max(part, align_up(L.seed.part_bytes, 256));
+      chunks = std::max(chunks, L.seed.n_chunks);
+    }
+  }
+  L.bufs_off = 0;
+  L.part_off = bufs;
+  L.cnt_off = L.part_off + part;
+  L.seed_s_off = L.cnt_off + align_up((size_t)chunks * nq * 4, 256);
+  L.seed_i_off = L.seed_s_off + (L.sp.on ? align_up((size_t)nq * k * 4, 256) : 0);
+  L.total = L.seed_i_off + (L.sp.on ? align_up((size_t)nq * k * 8, 256) : 0);
+  return L;
+}
+
+uq_status uq_search_asym_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes) {
+  if (!bytes) return UQ_ERR_INVALID_ARG;
+  if (nq < 0 || n < 0 || d < 1 || k < 1) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D || k > UQ_MAX_K || n >= (int64_t)0xffffffffLL) return UQ_ERR_UNSUPPORTED;
+  if (nq == 0 || n == 0) { *bytes = 0; return UQ_OK; }
+  const AsymLayout L = asym_layout(nq, n, d, k, device_sms());
+  if (!L.ok) return UQ_ERR_UNSUPPORTED;
+  *bytes = L.total;
+  return UQ_OK;
+}
+
+uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                         int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids, void* workspace,
+                         size_t workspace_bytes, uq_stream_t stream) {
+  g_launches = 0;
+  if (nq < 0 || n < 0 || d < 1 || k < 1 || ldq < d) return UQ_ERR_INVALID_ARG;
+  if ((nq > 0 && q8 == nullptr) || (n > 0 && nq > 0 && dbcodes == nullptr)) return UQ_ERR_INVALID_ARG;
+  if (dbcodes && !aligned16(dbcodes)) return UQ_ERR_INVALID_ARG;
+  if (d > UQ_MAX_D || k > UQ_MAX_K || n >= (int64_t)0xffffffffLL) return UQ_ERR_UNSUPPORTED;
+  if (nq == 0) return UQ_OK;
+  if (!out_scores || !out_ids) return UQ_ERR_INVALID_ARG;
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) return from_cuda(launch_merge_keys(nullptr, 0, nq, k, k, id_base, out_scores, out_ids, st));
+  const int sms = device_sms();
+  const AsymLayout L = asym_layout(nq, n, d, k, sms);
+  if (!L.ok) return UQ_ERR_UNSUPPORTED;
+  if (workspace_bytes < L.total || workspace == nullptr) return UQ_ERR_WORKSPACE;
+  if (((uintptr_t)workspace & 255u) != 0) return UQ_ERR_INVALID_ARG;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  uint32_t* bufs = reinterpret_cast<uint32_t*>(ws + L.bufs_off);
+  uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part_off);
+  int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.cnt_off);
+  const int32_t* thr0 = nullptr;
+  cudaError_t e;
+  if (L.sp.on) {
+    int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
+    int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
+    cudaEvent_t ev;
+    timer_begin(st, &ev, 1, (double)nq * (double)L.sp.rows);
+    e = launch_scan_tc2(nullptr, nq, dbcodes, L.sp.rows, d, k, L.seed, bufs, part, cnt, nullptr, 0, L.sp.stride, 0,
+                        st, nullptr, nullptr, q8, ldq);
+    timer_end(st, ev);
+    if (e != cudaSuccess) return UQ_ERR_CUDA;
+    e = launch_merge_keys(part, L.seed.n_chunks, nq, L.seed.cap, k, 0, seed_s, seed_i, st, cnt);
+    if (e != cudaSuccess) return UQ_ERR_CUDA;
+    thr0 = seed_s + (k - 1);   // k-th best sampled score: exact lower bound on D_k
+  }
+  cudaEvent_t ev;
+  timer_begin(st, &ev, 0, (double)nq * (double)n);
+  e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, thr0, k, 1, 0, st, nullptr, nullptr,
+                      q8, ldq);
+  timer_end(st, ev);
+  if (e != cudaSuccess) return UQ_ERR_CUDA;
+  return from_cuda(launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st,
+                                     cnt));
+}
+
 uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad_rows,
                          uq_stream_t stream) {
   g_launches = 0;

@@ -59,7 +59,8 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
 
 // Tensor-core scan on CTA pairs (scan_tc2.cu), used for query batches > 128;
 // op: operand kind, 0 = int8 (kind::i8), 1 = E2M1 (kind::mxf4, f32 accumulate).
-TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op);
+// sbound: bound on |score| (d for ternary queries; 127 d for int8 queries)
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op, int32_t sbound = 0);
 cudaError_t tc2_prof_read(unsigned long long* out48);
 TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op);
 // Seeding: histogram scan over rows {i * row_stride : i < n}, then per query
@@ -79,6 +80,10 @@ cudaError_t launch_seed_verify(const int64_t* out_ids, int64_t nq, int32_t k, co
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
-                            cudaStream_t st, const int32_t* qfail = nullptr, const int32_t* any_fail = nullptr);
+                            cudaStream_t st, const int32_t* qfail = nullptr, const int32_t* any_fail = nullptr,
+                            const int8_t* q8 = nullptr, int64_t ldq8 = 0);
+// int8 query quantisation (R15): per row scale 127 / max|u| (fp32), round half even
+cudaError_t launch_quantize_i8(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld, int8_t* out,
+                               int64_t ldo, cudaStream_t st);
 
 }  // namespace uq

@@ -111,6 +111,8 @@ struct Params {
   uint32_t* qbase;      // kHist: per query (hs << 16) | F, bin = (Delta - F) >> hs
   const int32_t* qfail; // top-k, optional (seed fallback pass): run only pair tiles with a failed query
   const int32_t* any_fail;  // optional: the launch is a no-op unless *any_fail
+  const int8_t* q8;     // optional (int8 engine): int8 queries [nq][ldq8] instead of ternary codes
+  int64_t ldq8;
   int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads,
                         // 8 cycle accounting, 16 no producer proxy fence
 };
@@ -260,6 +262,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
     }
     // ---- A: this CTA's 128 query codes, expanded (all threads) ----
     cluster_sync();  // previous item retired in both CTAs (A is read by the pair's MMAs)
+    if (OP == kOpI8 && p.q8 != nullptr) {
+      // single-operand search: A = the int8 queries themselves, in
+      // the K permutation of the DB expansion (chunk 2w + hb, byte 4 bb + j of
+      // a 128-dim block <-> dim 32 w + 8 j + bb + 4 hb), zero past d
+      for (int u = threadIdx.x; u < BM * NB * 8; u += kThreads) {
+        const int r = u / (NB * 8), kb = (u / 8) % NB, c = u % 8;
+        const int w = c >> 1, hb = c & 1;
+        uint32_t sw[8];
+        const int64_t qq = q0 + r;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int dim = kb * 128 + 32 * w + 4 * t + e;
+            const uint32_t b = (qq < p.nq && dim < p.d) ? (uint8_t)p.q8[qq * p.ldq8 + dim] : 0u;
+            word |= b << (8 * e);
+          }
+          sw[t] = word;
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) word |= ((sw[2 * j + hb] >> (8 * bb)) & 0xffu) << (8 * j);
+          o[bb] = word;
+        }
+        st_shared_v4(smem_u32(sA + (size_t)(kb * G::CPB + c) * A_LBO + (r >> 3) * SBO + (r & 7) * 16), o[0], o[1],
+                     o[2], o[3]);
+      }
+    } else
     for (int u = threadIdx.x; u < BM * NB; u += kThreads) {
       const int r = u / NB, kb = u % NB;
       uint4 qp = make_uint4(0, 0, 0, 0), qn = qp;
@@ -734,7 +768,7 @@ static int tc2_max_nb(int op) { return op == tc2::kOpF4 ? 12 : 8; }
 // Pairs: the query set is cut into 256-query pair tiles; each of the SMs/2
 // pairs gets one (pair tile, DB chunk) item when the tiles do not cover them.
 template <int OP>
-static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int mode) {
+static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int mode, int32_t sbound) {
   using G = tc2::Geo<OP>;
   TcPlan pl{};
   const int NB = blocks128(d);
@@ -746,7 +780,7 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   const int npairs = sms / 2;
   pl.n_qtiles = (int32_t)((nq + 2 * tc2::BM - 1) / (2 * tc2::BM));
   pl.cap = k + 2 * G::cw(mode);
-  const KeyFmt kf = make_keyfmt(d);
+  const KeyFmt kf = make_keyfmt(sbound);   // |score| <= sbound (d; 127 d for int8 queries)
   const int64_t lmax = ((int64_t)kf.rmask + 1) / G::BN * G::BN;
   const int64_t s_min = (n + lmax - 1) / lmax;
   int64_t s_cap = (n + 4 * G::BN - 1) / (4 * G::BN);
@@ -773,13 +807,14 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   return pl;
 }
 
-TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op) {
-  return op == tc2::kOpF4 ? plan_tc2_mode<tc2::kOpF4>(nq, n, d, k, sms, tc2::kModeTopK)
-                          : plan_tc2_mode<tc2::kOpI8>(nq, n, d, k, sms, tc2::kModeTopK);
+TcPlan plan_tc2(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op, int32_t sbound) {
+  if (sbound <= 0) sbound = d;
+  return op == tc2::kOpF4 ? plan_tc2_mode<tc2::kOpF4>(nq, n, d, k, sms, tc2::kModeTopK, sbound)
+                          : plan_tc2_mode<tc2::kOpI8>(nq, n, d, k, sms, tc2::kModeTopK, sbound);
 }
 TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int op) {
-  return op == tc2::kOpF4 ? plan_tc2_mode<tc2::kOpF4>(nq, n, d, k, sms, tc2::kModeHist)
-                          : plan_tc2_mode<tc2::kOpI8>(nq, n, d, k, sms, tc2::kModeHist);
+  return op == tc2::kOpF4 ? plan_tc2_mode<tc2::kOpF4>(nq, n, d, k, sms, tc2::kModeHist, d)
+                          : plan_tc2_mode<tc2::kOpI8>(nq, n, d, k, sms, tc2::kModeHist, d);
 }
 
 template <int NB, int MODE, int OP>
@@ -845,10 +880,12 @@ cudaError_t tc2_prof_read(unsigned long long* out48) {
 cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
-                            cudaStream_t st, const int32_t* qfail, const int32_t* any_fail) {
-  tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
+                            cudaStream_t st, const int32_t* qfail, const int32_t* any_fail, const int8_t* q8,
+                            int64_t ldq8) {
+  if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
+  tc2::Params p{q, nq, db, n, d, k, make_keyfmt(q8 ? 127 * d : d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
-                thr0_stride, row_stride, nullptr, 0.f, nullptr, qfail, any_fail, tc2_dbg()};
+                thr0_stride, row_stride, nullptr, 0.f, nullptr, qfail, any_fail, q8, ldq8, tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
 
@@ -867,7 +904,7 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
-                nullptr, 0, row_stride, ghist, z, qbase, nullptr, nullptr, tc2_dbg()};
+                nullptr, 0, row_stride, ghist, z, qbase, nullptr, nullptr, nullptr, 0, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, need, qbase, thr);

@@ -324,3 +324,80 @@ def test_seed_optimistic_fallback(uq, orc, monkeypatch, algo, opt, k, mode):
     stay bit-exact in every case."""
     monkeypatch.setenv("UQ_SEED_OPT", opt)
     _search_case(uq, orc, algo, 256, 128, 131072, 300, k, seed=5 + k, mode=mode)
+
+
+# --------------------------------------------------------------------------
+# Single-operand search (P:507-509): int8 queries x ternary DB, masked addition
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("d", [1, 10, 100, 384, 768, 1000, 1536])
+def test_quantize_i8_parity(uq, orc, dt, d):
+    rng = np.random.default_rng(d + 17)
+    n = 333
+    u = rng.standard_normal((n, d)).astype(np.float32)
+    u[: n // 4] = _tie_heavy(rng, n // 4, d)       # exact .5 products -> round-half-even
+    u[5] = 0.0                                      # zero row
+    ut = torch.from_numpy(u).to(dt)
+    host = ut.float().numpy()                       # exact widening of f16 / bf16
+    got = uq.quantize_i8(ut.cuda()).cpu().numpy()
+    assert np.array_equal(got, orc.quantize_i8(host))
+
+
+def _asym_case(uq, orc, d, x, n, nq, k, seed=0, mode="normal"):
+    rng = np.random.default_rng(seed)
+    if mode == "dup":
+        base = rng.standard_normal((max(1, n // 7), d)).astype(np.float32)
+        u_db = base[rng.integers(0, base.shape[0], size=n)]
+    elif mode == "ties":
+        u_db = _tie_heavy(rng, n, d)
+    else:
+        u_db = rng.standard_normal((n, d)).astype(np.float32)
+    u_q = rng.standard_normal((nq, d)).astype(np.float32)
+    if mode == "ties":
+        u_q = _tie_heavy(rng, nq, d)
+    o_db = orc.pack(orc.encode(u_db, x)) if n else np.zeros((0, 2 * orc.plane_bytes(d)), np.uint8)
+    q8 = orc.quantize_i8(u_q)
+    s, i = uq.search_asym(torch.from_numpy(q8).cuda(), torch.from_numpy(o_db).cuda(), d, k, id_base=7)
+    s_ref, i_ref = orc.knn_asym(q8, o_db, d, k, id_base=7)
+    s, i = s.cpu().numpy(), i.cpu().numpy()
+    assert np.array_equal(s, s_ref), (d, n, nq, k, np.argwhere(s != s_ref)[:5])
+    assert np.array_equal(i, i_ref), (d, n, nq, k, np.argwhere(i != i_ref)[:5])
+
+
+@pytest.mark.parametrize("n,nq,k", [(0, 3, 4), (1, 2, 1), (9, 4, 10), (257, 1, 10), (5000, 130, 10),
+                                    (3000, 7, 1024), (20000, 300, 100), (70001, 33, 10)])
+def test_search_asym_parity_shapes(uq, orc, n, nq, k):
+    _asym_case(uq, orc, 384, 192, n, nq, k, seed=n + nq + k)
+
+
+@pytest.mark.parametrize("d,x", [(10, 5), (100, 67), (768, 384), (1000, 667), (1024, 256), (129, 1)])
+def test_search_asym_parity_dims(uq, orc, d, x):
+    _asym_case(uq, orc, d, x, 6000, 150, 10, seed=d)
+
+
+@pytest.mark.parametrize("mode,n,k", [("dup", 131072, 100), ("ties", 100000, 10), ("normal", 70001, 1)])
+def test_search_asym_parity_seeded(uq, orc, mode, n, k):
+    """n >= 2^16: the exact 1/32-sample seed; massive score ties decided by id."""
+    _asym_case(uq, orc, 128, 64, n, 260, k, seed=13, mode=mode)
+
+
+def test_search_asym_full_size_c2_sampled(uq, orc):
+    """c2 at full size (N = 10^6, Q = 1000, k = 100): int8 queries from the GPU
+    quantiser (checked against the oracle's), top-k of 6 seeded queries against
+    the oracle's exhaustive masked-addition kNN over all 10^6 oracle-encoded rows."""
+    w = datagen.CONFIGS["c2"]
+    db = datagen.db(w, "cuda")
+    q = datagen.queries(w, "cuda")
+    dbc = uq.encode(db, w.x)
+    q8 = uq.quantize_i8(q)
+    s, i = uq.search_asym(q8, dbc, w.d, w.k)
+    db_h = db.cpu().numpy()
+    del db
+    o_db = orc.pack(orc.encode(db_h, w.x))
+    o_q8 = orc.quantize_i8(q.cpu().numpy())
+    assert np.array_equal(q8.cpu().numpy(), o_q8)
+    rng = np.random.default_rng(4)
+    qs = np.sort(rng.choice(w.nq, size=6, replace=False))
+    s_ref, i_ref = orc.knn_asym(o_q8[qs], o_db, w.d, w.k)
+    assert np.array_equal(s.cpu().numpy()[qs], s_ref)
+    assert np.array_equal(i.cpu().numpy()[qs], i_ref)
