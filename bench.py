@@ -228,7 +228,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(datagen.CONFIGS))
-    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc", "f4"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc", "f4", "asym"],
+                    help="asym: single-operand search (P:507-509), int8 queries x ternary DB")
     ap.add_argument("--n", type=int, default=None, help="override DB rows per GPU")
     ap.add_argument("--nq", type=int, default=None, help="override query batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -247,7 +248,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = datagen.CONFIGS[args.config].scaled(n=args.n, nq=args.nq)
-    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4}[args.algo]
+    asym = args.algo == "asym"
+    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4,
+            "asym": uq.ALGO_TCGEN05}[args.algo]
     n_loc, nq, d, x, k = w.n, w.nq, w.d, w.x, w.k
     id_base = rank * n_loc
 
@@ -273,14 +276,20 @@ def main():
     qc = torch.empty((nq, uq.code_bytes(d)), dtype=torch.uint8, device=dev)
     out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
            torch.empty((nq, k), dtype=torch.int64, device=dev))
-    ws = torch.empty(max(uq.search_workspace(nq, n_loc, d, k, algo), 1), dtype=torch.uint8,
-                     device=dev)
+    ws_bytes = uq.search_asym_workspace(nq, n_loc, d, k) if asym else uq.search_workspace(nq, n_loc, d, k, algo)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    q8 = torch.empty((nq, d), dtype=torch.int8, device=dev)
     launches = [0]
 
     def step(q_dev):
-        uq.encode(q_dev, x, out=qc)
-        launches[0] += uq.last_launches()
-        s, i = uq.search(qc, dbc, d, k, id_base=id_base, algo=algo, workspace=ws, out=out)
+        if asym:   # quantise the float queries to int8, masked-addition search
+            uq.quantize_i8(q_dev, out=q8)
+            launches[0] += uq.last_launches()
+            s, i = uq.search_asym(q8, dbc, d, k, id_base=id_base, workspace=ws, out=out)
+        else:
+            uq.encode(q_dev, x, out=qc)
+            launches[0] += uq.last_launches()
+            s, i = uq.search(qc, dbc, d, k, id_base=id_base, algo=algo, workspace=ws, out=out)
         launches[0] += uq.last_launches()
         if world > 1:
             sg, ig = allgather_lists(s, i)
@@ -361,6 +370,8 @@ def main():
     used_f4 = resolved == uq.ALGO_TC_FP4
     used_tc = resolved in (uq.ALGO_TCGEN05, uq.ALGO_TC_FP4)
     algo_name = "tcgen05-f4" if used_f4 else "tcgen05" if used_tc else "popc"
+    if asym:
+        used_f4, used_tc, algo_name = False, True, "tcgen05-asym-int8"
     # dominant kernel = the main scan (every DB row); per launch: nq * n_loc Delta evaluations
     scan_avg_s = (main_ms / max(main_n, 1)) * 1e-3
     evals_per_launch = main_evals / max(main_n, 1)
@@ -381,7 +392,9 @@ def main():
         achieved = ops / scan_avg_s / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": ("scan_tc2_kernel (CTA-pair int8 tcgen05 Delta GEMM + fused top-k)"
+                "kernel": ("scan_tc2_kernel<NB,0,0> (CTA-pair int8 tcgen05, int8 queries as the A operand: "
+                           "masked-addition scores + fused top-k)" if asym else
+                           "scan_tc2_kernel (CTA-pair int8 tcgen05 Delta GEMM + fused top-k)"
                            if nq > 128 and d <= 1024 else
                            "scan_tc_kernel (int8 tcgen05 Delta GEMM + fused top-k)"),
                 "peak_source": f"2 x bf16_tflops of {peaks_src} MEASURED_PEAKS.json (int8 = 2x bf16 nominal)",

@@ -171,8 +171,9 @@ uq_status uq_quantize_i8(const void* u, uq_dtype dt, int64_t n, int32_t d, int64
  * (INT32_MIN, -1).
  *   q8 [nq][ldq] int8 (device), ldq >= d; dbcodes [n][code_bytes(d)] (16-B
  *   aligned); workspace >= uq_search_asym_workspace() bytes, 256-B aligned.
- * Runs on the int8 tcgen05 CTA-pair engine (the queries are the A operand):
- * d <= 1024, otherwise UQ_ERR_UNSUPPORTED.  Other errors as uq_search.
+ * Runs on the int8 tcgen05 CTA-pair engine (the queries are the A operand)
+ * with the same verified optimistic seeding as uq_search: d <= 1024,
+ * otherwise UQ_ERR_UNSUPPORTED.  Other errors as uq_search.
  */
 uq_status uq_search_asym_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes);
 uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, int64_t n,

@@ -471,37 +471,32 @@ uq_status uq_quantize_i8(const void* u, uq_dtype dt, int64_t n, int32_t d, int64
 
 // ---- single-operand search: int8 queries x ternary database ----
 // Runs on the int8 CTA-pair engine with the queries as the A operand; scores
-// |S| <= 127 d set the key format.  Seeding: the exact k-th best of a 1/32
-// sample (a top-k scan of the sample + merge), as for the other engines.
+// |S| <= 127 d set the key format.  Seeding as the symmetric pair engines: a
+// score histogram of a 1/16 sample -> optimistic bound, verified after the
+// merge, exact fallback pass for the queries that fail.
 struct AsymLayout {
   bool ok;
-  TcPlan main, seed;
+  TcPlan main;
   SeedPlan sp;
-  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, total;
+  int32_t need;
+  size_t bufs_off, part_off, cnt_off, thr_off, hist_off, qbase_off, fail_off, total;
 };
 static AsymLayout asym_layout(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   AsymLayout L{};
   L.main = plan_tc2(nq, n, d, k, sms, 0, 127 * d);
   L.ok = L.main.ok;
   if (!L.ok) return L;
-  L.sp = plan_seed(n, k, false);
-  size_t bufs = align_up(L.main.buf_bytes, 256), part = align_up(L.main.part_bytes, 256);
-  int64_t chunks = L.main.n_chunks;
-  if (L.sp.on) {
-    L.seed = plan_tc2(nq, L.sp.rows, d, k, sms, 0, 127 * d);
-    if (!L.seed.ok) { L.sp.on = false; }
-    else {
-      bufs = std::max(bufs, align_up(L.seed.buf_bytes, 256));
-      part = std::max(part, align_up(L.seed.part_bytes, 256));
-      chunks = std::max(chunks, L.seed.n_chunks);
-    }
-  }
+  L.sp = plan_seed(n, k, true);
+  L.need = L.sp.on ? seed_need(k, L.sp.stride) : k;
+  const bool s = L.sp.on;
   L.bufs_off = 0;
-  L.part_off = bufs;
-  L.cnt_off = L.part_off + part;
-  L.seed_s_off = L.cnt_off + align_up((size_t)chunks * nq * 4, 256);
-  L.seed_i_off = L.seed_s_off + (L.sp.on ? align_up((size_t)nq * k * 4, 256) : 0);
-  L.total = L.seed_i_off + (L.sp.on ? align_up((size_t)nq * k * 8, 256) : 0);
+  L.part_off = align_up(L.main.buf_bytes, 256);
+  L.cnt_off = L.part_off + align_up(L.main.part_bytes, 256);
+  L.thr_off = L.cnt_off + align_up((size_t)L.main.n_chunks * nq * 4, 256);
+  L.hist_off = L.thr_off + (s ? align_up((size_t)nq * 4, 256) : 0);
+  L.qbase_off = L.hist_off + (s ? align_up((size_t)nq * 128 * 4, 256) : 0);
+  L.fail_off = L.qbase_off + (s ? align_up((size_t)nq * 4, 256) : 0);
+  L.total = L.fail_off + (s ? align_up((size_t)(nq + 1) * 4, 256) : 0);
   return L;
 }
 
@@ -537,29 +532,40 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
   uint32_t* bufs = reinterpret_cast<uint32_t*>(ws + L.bufs_off);
   uint64_t* part = reinterpret_cast<uint64_t*>(ws + L.part_off);
   int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.cnt_off);
+  int32_t* thr = reinterpret_cast<int32_t*>(ws + L.thr_off);
   const int32_t* thr0 = nullptr;
   cudaError_t e;
   if (L.sp.on) {
-    int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
-    int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
+    uint32_t* ghist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
+    uint32_t* qbase = reinterpret_cast<uint32_t*>(ws + L.qbase_off);
+    if (cudaMemsetAsync(ghist, 0, (size_t)nq * 128 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)L.sp.rows);
-    e = launch_scan_tc2(nullptr, nq, dbcodes, L.sp.rows, d, k, L.seed, bufs, part, cnt, nullptr, 0, L.sp.stride, 0,
-                        st, nullptr, nullptr, q8, ldq);
+    e = launch_seed_tc2_hist(nullptr, nq, dbcodes, L.sp.rows, d, k, L.need, L.sp.stride, ghist, qbase, thr, sms, 0,
+                             st, q8, ldq);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
-    e = launch_merge_keys(part, L.seed.n_chunks, nq, L.seed.cap, k, 0, seed_s, seed_i, st, cnt);
-    if (e != cudaSuccess) return UQ_ERR_CUDA;
-    thr0 = seed_s + (k - 1);   // k-th best sampled score: exact lower bound on D_k
+    thr0 = thr;
   }
   cudaEvent_t ev;
   timer_begin(st, &ev, 0, (double)nq * (double)n);
-  e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, thr0, k, 1, 0, st, nullptr, nullptr,
+  e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, thr0, 1, 1, 0, st, nullptr, nullptr,
                       q8, ldq);
   timer_end(st, ev);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
+  e = launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st, cnt);
+  if (e != cudaSuccess || !(L.sp.on && L.need < k)) return from_cuda(e);
+  // optimistic seeds: re-search the queries with fewer than k rows above their bound
+  int32_t* fail = reinterpret_cast<int32_t*>(ws + L.fail_off);
+  int32_t* any = fail + nq;
+  if (cudaMemsetAsync(any, 0, 4, st) != cudaSuccess) return UQ_ERR_CUDA;
+  e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
+  if (e != cudaSuccess) return UQ_ERR_CUDA;
+  e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, nullptr, 0, 1, 0, st, fail, any, q8,
+                      ldq);
+  if (e != cudaSuccess) return UQ_ERR_CUDA;
   return from_cuda(launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st,
-                                     cnt));
+                                     cnt, fail, any));
 }
 
 uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad_rows,

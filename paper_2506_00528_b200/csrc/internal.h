@@ -69,7 +69,8 @@ TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int o
 // optimistic bound, checked after the main scan by launch_seed_verify.
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
-                                 int32_t* thr, int sms, int op, cudaStream_t st);
+                                 int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8 = nullptr,
+                                 int64_t ldq8 = 0);
 // After a search with optimistic seeds: fail[q] = 1 iff q was filtered
 // (thr[q] != INT32_MIN) and fewer than k rows passed (its k-th result is
 // padding); *any |= 1 if some query failed (*any must be zero on entry).

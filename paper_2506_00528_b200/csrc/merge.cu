@@ -18,7 +18,7 @@ namespace uq {
 
 constexpr int kMergeThreads = 256;
 constexpr int kMergeWarps = kMergeThreads / 32;
-constexpr int kMergeMaxLists = 1024;   // counted lists gathered compactly up to this many
+constexpr int kMergeMaxLists = 2048;   // counted lists gathered compactly up to this many
 
 struct MergeParams {
   // source (a): keys [lists][nq][k]; source (b): scores/ids [lists][nq][k]

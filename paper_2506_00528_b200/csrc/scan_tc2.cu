@@ -443,21 +443,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         // that ~4k unrelated sample rows still clear it): the count above any
         // bin edge stays a lower bound, and almost every score costs one compare.
         int floor_m1 = 0x7fffffff;
-        int nnz = 0;
+        int top = 0;   // bound on any score of this query: nnz(q) (ternary) or sum |q_i| (int8)
         if (qme < p.nq) {
-          const uint8_t* qc = p.q + qme * cb;
-          for (int b = 0; b < NB; ++b) {
-            const uint4 a = *reinterpret_cast<const uint4*>(qc + b * 16);
-            const uint4 c = *reinterpret_cast<const uint4*>(qc + pb + b * 16);
-            nnz += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(c.x) + __popc(c.y) +
-                   __popc(c.z) + __popc(c.w);
+          if (OP == kOpI8 && p.q8 != nullptr) {
+            // int8 query (single-operand search): unrelated rows' scores have
+            // sigma ~ |q|_2 sqrt(x/d); x/d = 1/2 assumed for the floor (only
+            // the seed's efficiency depends on it)
+            int64_t s2 = 0;
+            for (int i = 0; i < p.d; ++i) {
+              const int v = p.q8[qme * p.ldq8 + i];
+              s2 += v * v;
+              top += v < 0 ? -v : v;
+            }
+            const float sigma = sqrtf(0.5f * (float)s2);
+            floor_m1 = max(0, (int)(p.zfloor * sigma)) - 1;
+            // bins up to 32 sigma above the floor (sum |q_i| is a far looser
+            // bound; higher scores land in the last bin, which keeps every
+            // "count >= edge" a valid lower bound)
+            top = min(top, floor_m1 + 1 + (int)(32.f * sigma) + 1);
+          } else {
+            const uint8_t* qc = p.q + qme * cb;
+            for (int b = 0; b < NB; ++b) {
+              const uint4 a = *reinterpret_cast<const uint4*>(qc + b * 16);
+              const uint4 c = *reinterpret_cast<const uint4*>(qc + pb + b * 16);
+              top += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(c.x) + __popc(c.y) +
+                     __popc(c.z) + __popc(c.w);
+            }
+            floor_m1 = max(0, (int)(p.zfloor * (float)top * rsqrtf((float)p.d))) - 1;
           }
-          floor_m1 = max(0, (int)(p.zfloor * (float)nnz * rsqrtf((float)p.d))) - 1;
         }
-        // bins of width 2^hs_q from F = floor_m1 + 1 up to nnz(q) >= any Delta
+        // bins of width 2^hs_q from F = floor_m1 + 1 up to top >= any score
         int hs_q = 0;
         if (qme < p.nq) {
-          const int range = max(nnz - floor_m1, 1);   // Delta in [F, nnz]: range values
+          const int range = max(top - floor_m1, 1);   // scores in [F, top]: range values
           hs_q = range > kHistBins ? 32 - __clz(range - 1) - 7 : 0;
           if (h == 0) p.qbase[qme] = ((uint32_t)hs_q << 16) | (uint32_t)(floor_m1 + 1);
         }
@@ -894,7 +912,8 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
 // (left zero on exit).
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
-                                 int32_t* thr, int sms, int op, cudaStream_t st) {
+                                 int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8, int64_t ldq8) {
+  if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;
   // floor: about 4k of n unrelated rows exceed it (Gaussian tail), z in [0, 4]
@@ -904,7 +923,7 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
-                nullptr, 0, row_stride, ghist, z, qbase, nullptr, nullptr, nullptr, 0, tc2_dbg()};
+                nullptr, 0, row_stride, ghist, z, qbase, nullptr, nullptr, q8, ldq8, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, need, qbase, thr);

@@ -401,3 +401,10 @@ def test_search_asym_full_size_c2_sampled(uq, orc):
     s_ref, i_ref = orc.knn_asym(o_q8[qs], o_db, w.d, w.k)
     assert np.array_equal(s.cpu().numpy()[qs], s_ref)
     assert np.array_equal(i.cpu().numpy()[qs], i_ref)
+
+
+@pytest.mark.parametrize("opt,k", [("0", 100), ("0.01", 500)])
+def test_search_asym_seed_fallback(uq, orc, monkeypatch, opt, k):
+    """Single-operand search with exact (0) and forced-failing (0.01) seeds."""
+    monkeypatch.setenv("UQ_SEED_OPT", opt)
+    _asym_case(uq, orc, 256, 128, 131072, 300, k, seed=21 + k)
