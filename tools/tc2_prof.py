@@ -19,18 +19,29 @@ nq = int(sys.argv[3]) if len(sys.argv) > 3 else None
 w = datagen.CONFIGS[cfg].scaled(n=n, nq=nq)
 db = uq.encode(datagen.db(w, "cuda"), w.x)
 q = uq.encode(datagen.queries(w, "cuda"), w.x)
-ALGO = uq.ALGO_TC_FP4 if os.environ.get("UQ_PROF_ALGO", "f4") == "f4" else uq.ALGO_TCGEN05
-ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, ALGO), dtype=torch.uint8, device="cuda")
+MODE = os.environ.get("UQ_PROF_ALGO", "f4")   # f4 | tc | asym
+ALGO = uq.ALGO_TC_FP4 if MODE == "f4" else uq.ALGO_TCGEN05
+if MODE == "asym":
+    q8 = uq.quantize_i8(datagen.queries(w, "cuda"))
+    ws = torch.empty(uq.search_asym_workspace(w.nq, w.n, w.d, w.k), dtype=torch.uint8, device="cuda")
+else:
+    ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, ALGO), dtype=torch.uint8, device="cuda")
+
+
+def run():
+    if MODE == "asym":
+        return uq.search_asym(q8, db, w.d, w.k, workspace=ws)
+    return uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws)
 L = uq._L
 L.uq_debug_tc2_prof.argtypes = [ctypes.c_void_p]
 buf = (ctypes.c_ulonglong * 48)()
 for _ in range(2):
-    uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws)
+    run()
 torch.cuda.synchronize()
 L.uq_debug_tc2_prof(buf)  # reset
 reps = 5
 for _ in range(reps):
-    uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws)
+    run()
 torch.cuda.synchronize()
 L.uq_debug_tc2_prof(buf)
 c = list(buf)
