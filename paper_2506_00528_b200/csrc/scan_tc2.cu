@@ -109,6 +109,7 @@ struct Params {
   uint32_t* ghist;      // kHist: [nq][kHistBins]
   float zfloor;         // kHist: only Delta >= F = zfloor * nnz(q) / sqrt(d) is counted
   uint32_t* qbase;      // kHist: per query (hs << 16) | F, bin = (Delta - F) >> hs
+  float topsig;         // kHist: bins span [F, min(bound, F + topsig * sigma)]
   const int32_t* qfail; // top-k, optional (seed fallback pass): run only pair tiles with a failed query
   const int32_t* any_fail;  // optional: the launch is a no-op unless *any_fail
   const int8_t* q8;     // optional (int8 engine): int8 queries [nq][ldq8] instead of ternary codes
@@ -372,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           for (int bb = 0; bb < kBlkPerStage; ++bb) {
             const int kb = ks * kBlkPerStage + bb;
             if (kb < NB) {
-              if (!(p.dbg & 1) && r < BH) {
+              if (!(p.dbg & 1) && r < BH && !(issuer && (p.dbg & 512))) {   // (512: ablation, issuer skips its rows)
                 if (OP == kOpF4)
                   expand_block_store_f4(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(p.dbg & 32));
                 else
@@ -460,7 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
             // bins up to 32 sigma above the floor (sum |q_i| is a far looser
             // bound; higher scores land in the last bin, which keeps every
             // "count >= edge" a valid lower bound)
-            top = min(top, floor_m1 + 1 + (int)(32.f * sigma) + 1);
+            top = min(top, floor_m1 + 1 + (int)(p.topsig * sigma) + 1);
           } else {
             const uint8_t* qc = p.q + qme * cb;
             for (int b = 0; b < NB; ++b) {
@@ -469,7 +470,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
               top += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(c.x) + __popc(c.y) +
                      __popc(c.z) + __popc(c.w);
             }
-            floor_m1 = max(0, (int)(p.zfloor * (float)top * rsqrtf((float)p.d))) - 1;
+            const float sigma = (float)top * rsqrtf((float)p.d);
+            floor_m1 = max(0, (int)(p.zfloor * sigma)) - 1;
+            top = min(top, floor_m1 + 1 + (int)(p.topsig * sigma) + 1);
           }
         }
         // bins of width 2^hs_q from F = floor_m1 + 1 up to top >= any score
@@ -916,7 +919,7 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(q8 ? 127 * d : d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
-                thr0_stride, row_stride, nullptr, 0.f, nullptr, qfail, any_fail, q8, ldq8, tc2_dbg()};
+                thr0_stride, row_stride, nullptr, 0.f, nullptr, 0.f, qfail, any_fail, q8, ldq8, tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
 
@@ -933,10 +936,13 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   double ptail = 4.0 * (double)k / (double)(n > 0 ? n : 1);
   if (ptail > 0.5) ptail = 0.5;
   float z = inv_norm_cdf(1.0 - ptail);
+  // histogram bins span [F, min(score bound, F + 32 sigma)] (measured: narrower
+  // caps clamp c2's D_k into the last bin; sum |q_i| is far too loose for int8 queries)
+  const float topsig = 32.f;
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
-                nullptr, 0, row_stride, ghist, z, qbase, nullptr, nullptr, q8, ldq8, tc2_dbg()};
+                nullptr, 0, row_stride, ghist, z, qbase, topsig, nullptr, nullptr, q8, ldq8, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, need, qbase, thr);
