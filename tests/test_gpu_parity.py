@@ -408,3 +408,27 @@ def test_search_asym_seed_fallback(uq, orc, monkeypatch, opt, k):
     """Single-operand search with exact (0) and forced-failing (0.01) seeds."""
     monkeypatch.setenv("UQ_SEED_OPT", opt)
     _asym_case(uq, orc, 256, 128, 131072, 300, k, seed=21 + k)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_one_bit_baseline_is_x_equals_d(uq, orc, algo):
+    """1-bit quantisation (sign bits, Hamming distance) is the {d,d} EVP.
+    With x = d the search ranks rows by d - 2 * Hamming(sign bits) -- checked here
+    against a numpy popcount of the sign planes, independent of the oracle's kNN
+    (zero coordinates are avoided so every code has x = d non-zeros)."""
+    rng = np.random.default_rng(31)
+    d, n, nq, k = 256, 20000, 140, 20
+    u = rng.standard_normal((n + nq, d)).astype(np.float32)
+    u[u == 0] = 1e-3
+    codes = uq.encode(torch.from_numpy(u).cuda(), d)
+    db, q = codes[:n], codes[n:]
+    if algo in ("tc", "f4") and not _tc_supported(uq, nq, n, d, k, _algo(uq, algo)):
+        pytest.skip("shape unsupported")
+    s, i = uq.search(q, db, d, k, algo=_algo(uq, algo))
+    sign = (u > 0)
+    ham = (sign[n:, None, :] != sign[None, :n, :]).sum(-1)          # [nq][n]
+    delta = d - 2 * ham
+    for r in range(nq):
+        order = np.lexsort((np.arange(n), -delta[r]))[:k]
+        assert np.array_equal(i[r].cpu().numpy(), order)
+        assert np.array_equal(s[r].cpu().numpy(), delta[r][order])
