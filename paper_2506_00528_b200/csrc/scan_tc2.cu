@@ -61,6 +61,10 @@ constexpr int kOpI8 = 0, kOpF4 = 1;   // operand kind: int8 (kind::i8) / E2M1 (k
 //   f4: N = 240 (120 per CTA): two 240-column f32 accumulators leave TMEM
 //       columns [480, 512) for the (constant) scale factors; 64 B per row per
 //       block, so a stage of 3-4 blocks (384-512 dims) still carries 6-8 MMAs.
+#ifndef UQ_F4_MAX_BPS
+#define UQ_F4_MAX_BPS 8
+#endif
+constexpr int kF4MaxBps = UQ_F4_MAX_BPS;   // f4: at most this many 128-dim blocks per stage
 template <int OP> struct Geo {
   static constexpr int BN = OP == kOpF4 ? 240 : 256;   // UMMA N
   static constexpr int BH = BN / 2;                    // DB rows expanded per CTA
@@ -78,7 +82,7 @@ template <int OP> struct Geo {
   static constexpr int threads(int mode) { return (kProdWarps + 4 * sets(mode)) * 32; }
   static constexpr int cw(int mode) { return BN / sets(mode); }
   static constexpr int bps(int NB) {                   // 128-dim blocks per pipeline stage
-    return OP == kOpI8 ? 2 : (NB <= 4 ? NB : (NB + (NB + 3) / 4 - 1) / ((NB + 3) / 4));
+    return OP == kOpI8 ? 2 : (NB <= kF4MaxBps ? NB : (NB + (NB + kF4MaxBps - 1) / kF4MaxBps - 1) / ((NB + kF4MaxBps - 1) / kF4MaxBps));
   }
   static constexpr int stage_bytes(int NB) { return bps(NB) * BH * RB; }
 };
