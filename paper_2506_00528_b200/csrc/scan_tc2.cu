@@ -65,6 +65,11 @@ constexpr int kOpI8 = 0, kOpF4 = 1;   // operand kind: int8 (kind::i8) / E2M1 (k
 #define UQ_F4_MAX_BPS 8
 #endif
 constexpr int kF4MaxBps = UQ_F4_MAX_BPS;   // f4: at most this many 128-dim blocks per stage
+constexpr int i8_max_bps(int NB) {
+  // two stages beside the resident query tile and the seeding histogram (32 KB)
+  const int fit = (227 * 1024 - 128 * NB * 128 - 32 * 1024 - 2048) / (2 * 128 * 128);
+  return fit < 4 ? (fit < 1 ? 1 : fit) : 4;
+}
 template <int OP> struct Geo {
   static constexpr int BN = OP == kOpF4 ? 240 : 256;   // UMMA N
   static constexpr int BH = BN / 2;                    // DB rows expanded per CTA
@@ -82,7 +87,10 @@ template <int OP> struct Geo {
   static constexpr int threads(int mode) { return (kProdWarps + 4 * sets(mode)) * 32; }
   static constexpr int cw(int mode) { return BN / sets(mode); }
   static constexpr int bps(int NB) {                   // 128-dim blocks per pipeline stage
-    return OP == kOpI8 ? 2 : (NB <= kF4MaxBps ? NB : (NB + (NB + kF4MaxBps - 1) / kF4MaxBps - 1) / ((NB + kF4MaxBps - 1) / kF4MaxBps));
+    // at most mx blocks per stage, split evenly over the fewest stages; int8:
+    // mx <= 4 and two stages must fit beside the resident query tile
+    const int mx = OP == kOpI8 ? i8_max_bps(NB) : kF4MaxBps;
+    return NB <= mx ? NB : (NB + (NB + mx - 1) / mx - 1) / ((NB + mx - 1) / mx);
   }
   static constexpr int stage_bytes(int NB) { return bps(NB) * BH * RB; }
 };

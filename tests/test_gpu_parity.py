@@ -432,3 +432,10 @@ def test_one_bit_baseline_is_x_equals_d(uq, orc, algo):
         order = np.lexsort((np.arange(n), -delta[r]))[:k]
         assert np.array_equal(i[r].cpu().numpy(), order)
         assert np.array_equal(s[r].cpu().numpy(), delta[r][order])
+
+
+@pytest.mark.parametrize("d,x", [(1024, 512), (1000, 500)])
+def test_search_asym_parity_wide_seeded(uq, orc, d, x):
+    """Widest int8-query tiles (128 x 1024 B resident) with the seeding histogram
+    in shared memory beside them: n >= 2^16 turns the seeding scan on."""
+    _asym_case(uq, orc, d, x, 70001, 140, 10, seed=d + 1, mode="dup")

@@ -1,6 +1,5 @@
 B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline"
-timeout 300 $B > gpurun_out/bq_c2.log 2>&1
-timeout 400 $B --config c3 > gpurun_out/bq_c3.log 2>&1
-timeout 400 $B --config c4 --n 12500000 > gpurun_out/bq_c4shard.log 2>&1
-timeout 400 $B --config c5 --nq 1024 > gpurun_out/bq_c5q1024.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "f4" > gpurun_out/bq_pytest.log 2>&1; tail -1 gpurun_out/bq_pytest.log
+timeout 300 $B --algo tc > gpurun_out/bi_c2tc.log 2>&1
+timeout 300 $B --algo asym > gpurun_out/bi_c2asym.log 2>&1
+timeout 400 $B --algo asym --config c3 > gpurun_out/bi_c3asym.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "tc or asym" > gpurun_out/bi_pytest.log 2>&1; tail -1 gpurun_out/bi_pytest.log
