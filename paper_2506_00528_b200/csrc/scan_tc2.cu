@@ -959,8 +959,10 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;
-  // floor: about 4k of n unrelated rows exceed it (Gaussian tail), z in [0, 4]
-  double ptail = 4.0 * (double)k / (double)(n > 0 ? n : 1);
+  // floor: about 4 * need of the n sampled unrelated rows exceed it (Gaussian
+  // tail), z in [0, 4]; only the rows above the final bound matter, so a
+  // higher floor just skips counting (and the SMEM atomics of) the bulk
+  double ptail = 4.0 * (double)need / (double)(n > 0 ? n : 1);
   if (ptail > 0.5) ptail = 0.5;
   float z = inv_norm_cdf(1.0 - ptail);
   // histogram bins span [F, min(score bound, F + 32 sigma)] (measured: narrower
