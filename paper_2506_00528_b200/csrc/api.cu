@@ -153,9 +153,16 @@ static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
     return e ? atoi(e) : -1;
   }();
   int seed_div = div_env >= 0 ? div_env : (hist ? 16 : 32);
-  // large databases: max(2^17, 4096 k) sampled rows already bound D_k tightly
-  // (measured on c3 / c5: larger samples only lengthen the seeding scan)
-  const int64_t cap = std::max<int64_t>((int64_t)1 << 17, (int64_t)4096 * k);
+  // large databases: max(2^17, 1024 k) sampled rows already bound D_k tightly
+  // (measured on c3 / c4 / c5: larger samples only lengthen the seeding scan)
+  // sampled rows per unit of k (override: UQ_SEED_CAPK).  With verified
+  // optimistic bounds a smaller sample suffices: c4 shard seeding 9.4 -> 3.0 ms
+  // for +1 ms of main scan at 1024 k (4096 k: the exact-bound era's setting)
+  static const int64_t capk = [] {
+    const char* e = getenv("UQ_SEED_CAPK");
+    return e ? (int64_t)atoll(e) : (int64_t)1024;
+  }();
+  const int64_t cap = std::max<int64_t>((int64_t)1 << 17, capk * k);
   if (div_env < 0 && n / seed_div > cap) seed_div = (int)std::min<int64_t>(n / cap, INT32_MAX);
   if (seed_div <= 0) return sp;
   if (n < (int64_t)1 << 16) return sp;
