@@ -209,7 +209,7 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   L.seed_s_off = L.cnt_off + cnt_bytes;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
   L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * (hist ? 1 : k) * 4, 256) : 0);
   L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
-  L.qbase_off = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 128 * 4, 256) : 0);
+  L.qbase_off = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 256 * 4, 256) : 0);
   L.fail_off = L.qbase_off + (sp.on && hist ? align_up((size_t)nq * 4, 256) : 0);   // [nq] u32 bin bases
   L.total = L.fail_off + (sp.on && hist ? align_up((size_t)(nq + 1) * 4, 256) : 0);  // [nq] fail + any
   return L;
@@ -396,7 +396,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     int32_t* thr = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
     uint32_t* ghist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
     uint32_t* qbase = reinterpret_cast<uint32_t*>(ws + L.qbase_off);
-    if (cudaMemsetAsync(ghist, 0, (size_t)nq * 128 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
+    if (cudaMemsetAsync(ghist, 0, (size_t)nq * 256 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)sp.rows);
     cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, need, sp.stride, ghist, qbase, thr,
@@ -501,7 +501,7 @@ static AsymLayout asym_layout(int64_t nq, int64_t n, int32_t d, int32_t k, int s
   L.cnt_off = L.part_off + align_up(L.main.part_bytes, 256);
   L.thr_off = L.cnt_off + align_up((size_t)L.main.n_chunks * nq * 4, 256);
   L.hist_off = L.thr_off + (s ? align_up((size_t)nq * 4, 256) : 0);
-  L.qbase_off = L.hist_off + (s ? align_up((size_t)nq * 128 * 4, 256) : 0);
+  L.qbase_off = L.hist_off + (s ? align_up((size_t)nq * 256 * 4, 256) : 0);
   L.fail_off = L.qbase_off + (s ? align_up((size_t)nq * 4, 256) : 0);
   L.total = L.fail_off + (s ? align_up((size_t)(nq + 1) * 4, 256) : 0);
   return L;
@@ -545,7 +545,7 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
   if (L.sp.on) {
     uint32_t* ghist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
     uint32_t* qbase = reinterpret_cast<uint32_t*>(ws + L.qbase_off);
-    if (cudaMemsetAsync(ghist, 0, (size_t)nq * 128 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
+    if (cudaMemsetAsync(ghist, 0, (size_t)nq * 256 * 4, st) != cudaSuccess) return UQ_ERR_CUDA;
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)L.sp.rows);
     e = launch_seed_tc2_hist(nullptr, nq, dbcodes, L.sp.rows, d, k, L.need, L.sp.stride, ghist, qbase, thr, sms, 0,

@@ -95,8 +95,12 @@ template <int OP> struct Geo {
   static constexpr int stage_bytes(int NB) { return bps(NB) * BH * RB; }
 };
 constexpr int kF4Bias = 0x4B400000;   // f32 bits of 1.5 * 2^23: (float)(v) + 1.5*2^23 has bits kF4Bias + v
-constexpr int kHistBins = 128;
-constexpr int kHistBytes = (kHistBins / 2) * BM * 4;   // [64 words][128 queries], two u16 counts per word
+// Seeding histogram: 256 bins where shared memory allows (E2M1, d <= 768: a
+// finer bound, fewer main-scan candidates), else 128; two u16 counts per word,
+// [bins/2 words][128 queries].  The global histogram is always [nq][256].
+constexpr int kHistBinsMax = 256;
+constexpr int hist_bins(int OP, int NB) { return (OP == kOpF4 && NB <= 6) ? 256 : 128; }
+constexpr int hist_bytes(int OP, int NB) { return (hist_bins(OP, NB) / 2) * BM * 4; }
 constexpr int kModeTopK = 0, kModeHist = 1;
 
 struct Params {
@@ -118,7 +122,7 @@ struct Params {
   const int32_t* thr0;  // optional per-query seed D_k (rows with Delta < D_k cannot matter)
   int32_t thr0_stride;
   int64_t row_stride;
-  uint32_t* ghist;      // kHist: [nq][kHistBins]
+  uint32_t* ghist;      // kHist: [nq][kHistBinsMax]
   float zfloor;         // kHist: only Delta >= F = zfloor * nnz(q) / sqrt(d) is counted
   uint32_t* qbase;      // kHist: per query (hs << 16) | F, bin = (Delta - F) >> hs
   float topsig;         // kHist: bins span [F, min(bound, F + topsig * sigma)]
@@ -179,9 +183,10 @@ __device__ __forceinline__ Item decode_item(const Params& p, int64_t i) {
 }
 
 // kHist: add this thread's histogram column (query `qi`) to the global one and clear it
+template <int HB>
 __device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* g) {
 #pragma unroll 4
-  for (int w = 0; w < kHistBins / 2; ++w) {
+  for (int w = 0; w < HB / 2; ++w) {
     uint32_t* cell = s_hist + w * BM + col;
     const uint32_t v = atomicExch(cell, 0u);
     if (g != nullptr) {   // (timing ablation UQ_TC_ABLATE & 64 passes g = nullptr)
@@ -197,6 +202,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   using G = Geo<OP>;
   constexpr int BN = G::BN, BH = G::BH;
+  constexpr int kHistBins = hist_bins(OP, NB);
+  constexpr int kHistBytes = hist_bytes(OP, NB);
+  constexpr int kHistLog = kHistBins == 256 ? 8 : 7;
   constexpr int kEpiSets = G::sets(MODE);
   constexpr int kThreads = G::threads(MODE);
   constexpr int kBlkPerStage = G::bps(NB);
@@ -500,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         int hs_q = 0;
         if (qme < p.nq) {
           const int range = max(top - floor_m1, 1);   // scores in [F, top]: range values
-          hs_q = range > kHistBins ? 32 - __clz(range - 1) - 7 : 0;
+          hs_q = range > kHistBins ? 32 - __clz(range - 1) - kHistLog : 0;
           if (h == 0) p.qbase[qme] = ((uint32_t)hs_q << 16) | (uint32_t)(floor_m1 + 1);
         }
         const bool raw = OP == kOpF4 && __all_sync(kFull, floor_m1 >= 0);
@@ -569,13 +577,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           // u16 counters: flush every 128 tiles (128 * 256 rows < 65536 per query)
           if ((tile & 127) == 127) {
             named_bar_sync(1 + quarter, 32 * kEpiSets);  // all sets' warps of this quarter
-            if (h == 0) hist_flush(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBins : nullptr);
+            if (h == 0) hist_flush<kHistBins>(s_hist, col, qme < p.nq ? p.ghist + (size_t)qme * kHistBinsMax : nullptr);
             named_bar_sync(1 + quarter, 32 * kEpiSets);
           }
         }
         named_bar_sync(1 + quarter, 32 * kEpiSets);
         const long long tf0 = (p.dbg & 8) ? clk() : 0;
-        if (h == 0) hist_flush(s_hist, col, (qme < p.nq && !(p.dbg & 64)) ? p.ghist + (size_t)qme * kHistBins : nullptr);
+        if (h == 0) hist_flush<kHistBins>(s_hist, col, (qme < p.nq && !(p.dbg & 64)) ? p.ghist + (size_t)qme * kHistBinsMax : nullptr);
         named_bar_sync(1 + quarter, 32 * kEpiSets);
         if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[18], (unsigned long long)(clk() - tf0));
         if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[19], 1ull);
@@ -755,28 +763,42 @@ __global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, con
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (q >= nq) return;
-  uint4* g = reinterpret_cast<uint4*>(ghist + (size_t)q * kHistBins) + lane;
-  const uint4 h = *g;
-  *g = make_uint4(0u, 0u, 0u, 0u);
-  const uint32_t tot = h.x + h.y + h.z + h.w;
+  // lane l: bins 8l .. 8l+7
+  uint4* g = reinterpret_cast<uint4*>(ghist + (size_t)q * kHistBinsMax) + 2 * lane;
+  const uint4 h0 = g[0], h1 = g[1];
+  g[0] = make_uint4(0u, 0u, 0u, 0u);
+  g[1] = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t hb[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  uint32_t tot = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) tot += hb[j];
   uint32_t suf = tot;  // sum over lanes >= lane
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t t = __shfl_down_sync(kFull, suf, o);
     if (lane + o < 32) suf += t;
   }
-  // suffix sums of this lane's bins
-  const uint32_t s3 = suf - tot + h.w, s2 = s3 + h.z, s1 = s2 + h.y, s0 = s1 + h.x;
-  const unsigned ok = __ballot_sync(kFull, s0 >= (uint32_t)k);
+  // suffix sums of this lane's bins: s[j] = sum of bins >= 8 lane + j
+  uint32_t sj[8];
+  uint32_t run = suf - tot;
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+    run += hb[j];
+    sj[j] = run;
+  }
+  const unsigned ok = __ballot_sync(kFull, sj[0] >= (uint32_t)k);
   if (ok == 0u) {
     if (lane == 0) thr[q] = INT32_MIN;
     return;
   }
   const int L = 31 - __clz(ok);
   if (lane == L) {
-    const int j = (s3 >= (uint32_t)k) ? 3 : (s2 >= (uint32_t)k) ? 2 : (s1 >= (uint32_t)k) ? 1 : 0;
+    int j = 0;
+#pragma unroll
+    for (int jj = 1; jj < 8; ++jj)
+      if (sj[jj] >= (uint32_t)k) j = jj;
     const uint32_t qb = qbase[q];
-    thr[q] = (int32_t)(qb & 0xffffu) + ((4 * L + j) << (qb >> 16));
+    thr[q] = (int32_t)(qb & 0xffffu) + ((8 * L + j) << (qb >> 16));
   }
 }
 
@@ -799,7 +821,7 @@ __global__ void seed_verify_kernel(const int64_t* out_ids, int64_t nq, int32_t k
 template <int OP>
 static int tc2_stages(int NB, int mode) {
   const int a_bytes = tc2::BM * NB * tc2::Geo<OP>::RB;
-  const int budget = 227 * 1024 - a_bytes - (mode == tc2::kModeHist ? tc2::kHistBytes : 0) - 2048;
+  const int budget = 227 * 1024 - a_bytes - (mode == tc2::kModeHist ? tc2::hist_bytes(OP, NB) : 0) - 2048;
   int s = budget / tc2::Geo<OP>::stage_bytes(NB);
   if (s > 6) s = 6;
   return s;
@@ -862,7 +884,7 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   const int64_t pairs = pl.n_items < npairs ? pl.n_items : npairs;
   pl.grid = (int32_t)(2 * pairs);
   pl.smem = 1024 + tc2::BM * NB * G::RB + pl.stages * G::stage_bytes(NB) +
-            (mode == tc2::kModeHist ? tc2::kHistBytes : 0) + (2 * pl.stages + 4) * 8 + 16;
+            (mode == tc2::kModeHist ? tc2::hist_bytes(OP, NB) : 0) + (2 * pl.stages + 4) * 8 + 16;
   pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * G::sets(mode) * tc2::BM * pl.cap * 4;
   pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * pl.cap * 8;
   return pl;

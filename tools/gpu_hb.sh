@@ -1,0 +1,7 @@
+B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline"
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "seed or search" > gpurun_out/hb_pytest.log 2>&1; tail -1 gpurun_out/hb_pytest.log
+timeout 300 $B > gpurun_out/hb_c2.log 2>&1
+timeout 300 $B --algo asym > gpurun_out/hb_c2asym.log 2>&1
+timeout 400 $B --config c5 --nq 1024 > gpurun_out/hb_c5q1024.log 2>&1
+timeout 400 $B --config c3 > gpurun_out/hb_c3.log 2>&1
+UQ_TC_ABLATE=0 timeout 300 python tools/tc2_prof.py c2 > gpurun_out/hb_prof.log 2>&1
