@@ -233,6 +233,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override DB rows per GPU")
     ap.add_argument("--nq", type=int, default=None, help="override query batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: NCCL allgather + merge, or one merge kernel reading every rank's lists "
+                         "from symmetric (peer-mapped) memory")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = _dist()
@@ -243,7 +246,7 @@ def main():
         return rc
 
     import paper_2506_00528_b200 as uq
-    from paper_2506_00528_b200.parallel import allgather_lists
+    from paper_2506_00528_b200.parallel import PeerExchange, allgather_lists
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -281,6 +284,8 @@ def main():
     q8 = torch.empty((nq, d), dtype=torch.int8, device=dev)
     launches = [0]
 
+    peer = PeerExchange(nq, k, dev) if (world > 1 and args.exchange == "peer") else None
+
     def step(q_dev, o=None):
         o = out if o is None else o
         if asym:   # quantise the float queries to int8, masked-addition search
@@ -292,7 +297,9 @@ def main():
             launches[0] += uq.last_launches()
             s, i = uq.search(qc, dbc, d, k, id_base=id_base, algo=algo, workspace=ws, out=o)
         launches[0] += uq.last_launches()
-        if world > 1:
+        if world > 1 and peer is not None:
+            s, i = peer.merge(s, i)
+        elif world > 1:
             sg, ig = allgather_lists(s, i)
             s, i = uq.merge_topk(sg, ig, k)
             launches[0] += uq.last_launches()
@@ -472,7 +479,8 @@ def main():
         "data": "synthetic",
         "config": {"workload": _workload_desc(w), "db_rows_per_gpu": n_loc, "global_db_rows": n_loc * world,
                    "queries": nq, "k": k, "algo": algo_name,
-                   "parallelism": f"db-shard x{world} + allgather/merge" if world > 1 else "single GPU",
+                   "parallelism": (f"db-shard x{world} + " + ("peer-memory merge" if peer is not None else
+                                                               "NCCL allgather + merge")) if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2: {n_loc * uq.code_bytes(d) / 1e6:.0f} MB of DB codes per GPU scanned per step"},
         "qps": nq * args.steps / (ms * 1e-3),
         "roofline": roof,

@@ -141,6 +141,19 @@ uq_status uq_merge_topk(const int32_t* scores, const int64_t* ids, int32_t g, in
                         int32_t k, int32_t* out_scores, int64_t* out_ids, uq_stream_t stream);
 
 /*
+ * uq_merge_topk_ptrs -- uq_merge_topk over g lists given by base pointers:
+ * score_ptrs / id_ptrs are DEVICE arrays of g device pointers, list r being
+ * scores [nq][k] int32 / ids [nq][k] int64 at score_ptrs[r] / id_ptrs[r].  The
+ * pointers may be peer-mapped buffers of other GPUs (CUDA IPC / symmetric
+ * memory over NVLink): the exchange step of the G-GPU search then is this one
+ * kernel reading every rank's lists directly, with no staging allgather.
+ * Same ordering, padding and errors as uq_merge_topk.
+ */
+uq_status uq_merge_topk_ptrs(const int32_t* const* score_ptrs, const int64_t* const* id_ptrs, int32_t g,
+                             int64_t nq, int32_t k, int32_t* out_scores, int64_t* out_ids,
+                             uq_stream_t stream);
+
+/*
  * uq_check_codes -- count rows that are not valid packed ternary codes: some
  * position set in both planes (pos AND neg != 0), or a pad bit (i >= d) set.
  * *bad_rows is a DEVICE uint64 scalar that the call overwrites.

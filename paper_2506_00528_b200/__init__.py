@@ -18,7 +18,7 @@ __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
     "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05", "ALGO_TC_FP4",
     "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex", "rerank",
-    "quantize_i8", "search_asym", "search_asym_workspace",
+    "quantize_i8", "search_asym", "search_asym_workspace", "merge_topk_ptrs",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -54,6 +54,7 @@ def _load():
     L.uq_rerank.argtypes = [vp, i32, i64, i64, vp, i64, i64, i32, vp, i32, i32, vp, vp, vp]
     L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
     L.uq_quantize_i8.argtypes = [vp, i32, i64, i32, i64, vp, i64, vp]
+    L.uq_merge_topk_ptrs.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
     L.uq_search_asym_workspace.argtypes = [i64, i64, i32, i32, ctypes.POINTER(sz)]
     L.uq_search_asym.argtypes = [vp, i64, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
@@ -62,7 +63,8 @@ def _load():
     L.uq_timing_collect_ex.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64),
                                        ctypes.POINTER(ctypes.c_double)]
     for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_timing_collect_ex", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
-              "uq_check_codes", "uq_rerank", "uq_quantize_i8", "uq_search_asym_workspace", "uq_search_asym"):
+              "uq_check_codes", "uq_rerank", "uq_quantize_i8", "uq_search_asym_workspace", "uq_search_asym",
+              "uq_merge_topk_ptrs"):
         getattr(L, f).restype = i32
     return L
 
@@ -249,6 +251,24 @@ def merge_topk(scores_g: torch.Tensor, ids_g: torch.Tensor, k: int,
                torch.empty((nq, k), dtype=torch.int64, device=scores_g.device))
     _check("uq_merge_topk", _L.uq_merge_topk(_ptr(scores_g), _ptr(ids_g), g, nq, k, _ptr(out[0]),
                                              _ptr(out[1]), _stream(stream)))
+    return out
+
+
+def merge_topk_ptrs(score_ptrs: torch.Tensor, id_ptrs: torch.Tensor, nq: int, k: int,
+                    out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
+                    stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """uq_merge_topk_ptrs: merge g lists given as DEVICE int64 tensors of base
+    pointers (score_ptrs[r] -> int32 [nq][k], id_ptrs[r] -> int64 [nq][k]; peer-
+    mapped buffers of other GPUs allowed) into the k best per query."""
+    _dev(score_ptrs, "score_ptrs"); _dev(id_ptrs, "id_ptrs")
+    if score_ptrs.dtype != torch.int64 or id_ptrs.dtype != torch.int64 or score_ptrs.numel() != id_ptrs.numel():
+        raise ValueError("pointer arrays must be int64 device tensors of equal length")
+    g = score_ptrs.numel()
+    if out is None:
+        out = (torch.empty((nq, k), dtype=torch.int32, device=score_ptrs.device),
+               torch.empty((nq, k), dtype=torch.int64, device=score_ptrs.device))
+    _check("uq_merge_topk_ptrs", _L.uq_merge_topk_ptrs(_ptr(score_ptrs), _ptr(id_ptrs), g, nq, k, _ptr(out[0]),
+                                                       _ptr(out[1]), _stream(stream)))
     return out
 
 

@@ -447,6 +447,16 @@ uq_status uq_merge_topk(const int32_t* scores, const int64_t* ids, int32_t g, in
   return from_cuda(launch_merge_si(scores, ids, g, nq, k, out_scores, out_ids, (cudaStream_t)stream));
 }
 
+uq_status uq_merge_topk_ptrs(const int32_t* const* score_ptrs, const int64_t* const* id_ptrs, int32_t g,
+                             int64_t nq, int32_t k, int32_t* out_scores, int64_t* out_ids, uq_stream_t stream) {
+  g_launches = 0;
+  if (g < 0 || nq < 0 || k < 1) return UQ_ERR_INVALID_ARG;
+  if (k > UQ_MAX_K) return UQ_ERR_UNSUPPORTED;
+  if (nq == 0) return UQ_OK;
+  if (!out_scores || !out_ids || (g > 0 && (!score_ptrs || !id_ptrs))) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_merge_ptrs(score_ptrs, id_ptrs, g, nq, k, out_scores, out_ids, (cudaStream_t)stream));
+}
+
 uq_status uq_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, const void* db, int64_t n, int64_t ld,
                     int32_t d, const int64_t* cand, int32_t n_cand, int32_t k, float* out_cos, int64_t* out_ids,
                     uq_stream_t stream) {

@@ -29,6 +29,8 @@ cudaError_t launch_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, c
                           int64_t* out_ids, cudaStream_t st);
 cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
                             int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st);
+cudaError_t launch_merge_ptrs(const int32_t* const* score_ptrs, const int64_t* const* id_ptrs, int64_t lists,
+                              int64_t nq, int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st);
 
 // Popcount scan (scan_popc.cu).
 struct PopcPlan {

@@ -36,13 +36,23 @@ struct MergeParams {
   const int32_t* counts;  // source (a), optional: valid entries per list [lists][nq] (rest unread, empty)
   const int32_t* only;    // optional: merge only queries q with only[q] != 0 (seed fallback pass)
   const int32_t* any;     // optional: the whole launch is a no-op unless *any != 0
+  // source (b) through per-list base pointers (peer-mapped buffers of other
+  // GPUs: the merge reads every rank's [nq][k] lists directly over NVLink)
+  const int32_t* const* score_ptrs;
+  const int64_t* const* id_ptrs;
 };
 
 template <bool FROM_SI>
 __device__ __forceinline__ uint64_t cand_key(const MergeParams& p, int64_t q, int64_t i) {
   const int64_t l = i / p.kin, e = i % p.kin;
   const size_t off = ((size_t)l * p.nq + q) * p.kin + e;
-  if (FROM_SI) return global_key(p.scores[off], p.ids[off]);
+  if (FROM_SI) {
+    if (p.score_ptrs != nullptr) {
+      const size_t o = (size_t)q * p.kin + e;
+      return global_key(p.score_ptrs[l][o], p.id_ptrs[l][o]);
+    }
+    return global_key(p.scores[off], p.ids[off]);
+  }
   if (p.counts != nullptr && e >= p.counts[(size_t)l * p.nq + q]) return 0ull;
   return p.keys[off];
 }
@@ -226,13 +236,22 @@ static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
                               int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
                               const int32_t* counts, const int32_t* only, const int32_t* any) {
-  MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0, counts, only, any};
+  MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0, counts, only, any, nullptr,
+                nullptr};
   return launch_merge_common(p, false, st);
 }
 
 cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
                             int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
-  MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0, nullptr, nullptr, nullptr};
+  MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0, nullptr, nullptr, nullptr, nullptr,
+                nullptr};
+  return launch_merge_common(p, true, st);
+}
+
+cudaError_t launch_merge_ptrs(const int32_t* const* score_ptrs, const int64_t* const* id_ptrs, int64_t lists,
+                              int64_t nq, int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
+  MergeParams p{nullptr, nullptr, nullptr, lists, nq, k, k, 0, out_s, out_id, 0, nullptr, nullptr, nullptr,
+                score_ptrs, id_ptrs};
   return launch_merge_common(p, true, st);
 }
 

@@ -41,6 +41,42 @@ def allgather_lists(scores: torch.Tensor, ids: torch.Tensor, group=None):
     return sg.view(world, q, k), ig.view(world, q, k)
 
 
+class PeerExchange:
+    """Exchange + merge as ONE kernel over peer memory (NVLink / NVSwitch).
+
+    Each rank owns a symmetric-memory pair of [Q][k] buffers
+    (``torch.distributed._symmetric_memory``); every rank maps all peers'
+    buffers, so after a device-side barrier ``uq_merge_topk_ptrs`` reads every
+    rank's lists directly and merges them -- no staging allgather.  A second
+    barrier keeps a rank from overwriting its lists while peers still read them.
+    """
+
+    def __init__(self, nq: int, k: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+        if group is None:
+            group = dist.group.WORLD
+        self.nq, self.k = nq, k
+        self.s = symm.empty((nq, k), dtype=torch.int32, device=device)
+        self.i = symm.empty((nq, k), dtype=torch.int64, device=device)
+        self.hs = symm.rendezvous(self.s, group)
+        self.hi = symm.rendezvous(self.i, group)
+        world = self.hs.world_size
+        sb = [self.hs.get_buffer(r, (nq, k), torch.int32) for r in range(world)]
+        ib = [self.hi.get_buffer(r, (nq, k), torch.int64) for r in range(world)]
+        self.world = world
+        self.sptr = torch.tensor([t.data_ptr() for t in sb], dtype=torch.int64, device=device)
+        self.iptr = torch.tensor([t.data_ptr() for t in ib], dtype=torch.int64, device=device)
+
+    def merge(self, scores: torch.Tensor, ids: torch.Tensor):
+        import paper_2506_00528_b200 as uq
+        self.s.copy_(scores)
+        self.i.copy_(ids)
+        self.hs.barrier()          # every rank's lists are in its buffer
+        out = uq.merge_topk_ptrs(self.sptr, self.iptr, self.nq, self.k)
+        self.hs.barrier()          # every peer has finished reading
+        return out
+
+
 def sharded_search(qcodes: torch.Tensor, db_shard: torch.Tensor, d: int, k: int, id_base: int,
                    group=None, search_fn: Optional[Callable] = None,
                    merge_fn: Optional[Callable] = None, **search_kw):

@@ -439,3 +439,61 @@ def test_search_asym_parity_wide_seeded(uq, orc, d, x):
     """Widest int8-query tiles (128 x 1024 B resident) with the seeding histogram
     in shared memory beside them: n >= 2^16 turns the seeding scan on."""
     _asym_case(uq, orc, d, x, 70001, 140, 10, seed=d + 1, mode="dup")
+
+
+def test_merge_topk_ptrs_parity(uq, orc):
+    """uq_merge_topk_ptrs (the peer-memory exchange's merge) over G separately
+    allocated lists equals uq_merge_topk over the same lists stacked, and a
+    Python brute force."""
+    rng = np.random.default_rng(18)
+    g, nq, k = 6, 41, 23
+    lists_s, lists_i = [], []
+    for r in range(g):
+        sc = rng.integers(-30, 31, size=(nq, k)).astype(np.int32)
+        ids = np.stack([rng.permutation(1000)[:k] + 1000 * r for _ in range(nq)]).astype(np.int64)
+        if r == 2:
+            ids[:, 15:] = -1
+            sc[:, 15:] = np.iinfo(np.int32).min
+        lists_s.append(torch.from_numpy(sc).cuda())
+        lists_i.append(torch.from_numpy(ids).cuda())
+    sp = torch.tensor([t.data_ptr() for t in lists_s], dtype=torch.int64, device="cuda")
+    ip = torch.tensor([t.data_ptr() for t in lists_i], dtype=torch.int64, device="cuda")
+    s, i = uq.merge_topk_ptrs(sp, ip, nq, k)
+    s2, i2 = uq.merge_topk(torch.stack(lists_s), torch.stack(lists_i), k)
+    assert torch.equal(s, s2) and torch.equal(i, i2)
+    S = np.stack([t.cpu().numpy() for t in lists_s])
+    I = np.stack([t.cpu().numpy() for t in lists_i])
+    for q in range(nq):
+        cand = sorted([(int(S[r, q, j]), int(I[r, q, j])) for r in range(g) for j in range(k) if I[r, q, j] >= 0],
+                      key=lambda t: (-t[0], t[1]))[:k]
+        assert s[q].cpu().tolist() == [c[0] for c in cand] and i[q].cpu().tolist() == [c[1] for c in cand]
+
+
+def test_peer_exchange_world1(uq):
+    """The symmetric-memory exchange path end to end on a one-rank group (the
+    only topology a one-GPU test box has): rendezvous, barrier, merge over the
+    mapped buffer equals the local lists."""
+    import os
+    import torch.distributed as dist
+    from paper_2506_00528_b200.parallel import PeerExchange
+    owned = not dist.is_initialized()
+    if owned:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    rng = np.random.default_rng(5)
+    nq, k = 17, 9
+    s = torch.from_numpy(rng.integers(-9, 9, size=(nq, k)).astype(np.int32)).cuda()
+    i = torch.from_numpy(np.stack([rng.permutation(100)[:k] for _ in range(nq)]).astype(np.int64)).cuda()
+    try:
+        ex = PeerExchange(nq, k, torch.device("cuda:0"))
+    except Exception as e:   # symmetric memory unavailable in this build: nothing to exercise
+        pytest.skip(f"symmetric memory unavailable: {e}")
+    try:
+        ms, mi = ex.merge(s, i)
+        ref_s, ref_i = uq.merge_topk(s[None], i[None], k)
+        assert torch.equal(ms, ref_s) and torch.equal(mi, ref_i)
+    finally:
+        if owned:
+            torch.cuda.synchronize()
+            dist.destroy_process_group()
