@@ -93,8 +93,13 @@ static uq_algo resolve_algo(uq_algo algo, int64_t nq, int64_t n, int32_t d, int3
   // expansion) once a 256-query pair tile is more than half full.
   // small databases: the tensor engines' fixed per-CTA cost (TMEM allocation,
   // query-tile expansion, pipeline fill) exceeds a popcount scan of few rows
+  // Measured on c2 (N = 10^6, k = 100; profiles/r01/batch_sweep.jsonl): the
+  // popcount scan streams the codes at HBM speed for a few queries but is
+  // POPC-bound beyond that (0.15 ms per batch at Q = 1, 0.86 ms at Q = 16);
+  // the E2M1 pair engine costs ~0.32 ms per batch for any Q <= 256 (one pass
+  // of the database through a 256-query tile), so it wins from Q ~ 8 on.
   const bool big = n >= ((int64_t)1 << 16);
-  if (nq > 128 && big && plan_tc2(nq, n, d, k, sms, 1).ok) return UQ_ALGO_TC_FP4;
+  if (nq > 8 && big && plan_tc2(nq, n, d, k, sms, 1).ok) return UQ_ALGO_TC_FP4;
   if (tp.ok && nq >= 64 && big) return UQ_ALGO_TCGEN05;
   return UQ_ALGO_POPC;
 }
@@ -175,7 +180,8 @@ static SeedPlan plan_seed(int64_t n, int32_t k, bool hist) {
 }
 
 struct SearchLayout {
-  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, hist_off, qbase_off, fail_off, total;
+  size_t bufs_off, part_off, cnt_off, seed_s_off, seed_i_off, hist_off, qbase_off, fail_off, mscr_off, mscr_bytes,
+      total;
 };
 
 static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms,
@@ -191,7 +197,7 @@ static size_t engine_bytes(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t 
 }
 
 static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
-  SearchLayout L{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  SearchLayout L{};
   if (nq == 0 || n == 0) return L;
   size_t bufs = 0, part = engine_bytes(a, nq, n, d, k, sms, &bufs);
   const bool hist = hist_seed(a, nq, d);
@@ -211,7 +217,9 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
   L.qbase_off = L.hist_off + (sp.on && hist ? align_up((size_t)nq * 256 * 4, 256) : 0);
   L.fail_off = L.qbase_off + (sp.on && hist ? align_up((size_t)nq * 4, 256) : 0);   // [nq] u32 bin bases
-  L.total = L.fail_off + (sp.on && hist ? align_up((size_t)(nq + 1) * 4, 256) : 0);  // [nq] fail + any
+  L.mscr_off = L.fail_off + (sp.on && hist ? align_up((size_t)(nq + 1) * 4, 256) : 0);  // [nq] fail + any
+  L.mscr_bytes = merge_scratch_bytes(nq, k);   // two-level merge (few queries)
+  L.total = L.mscr_off + align_up(L.mscr_bytes, 256);
   return L;
 }
 
@@ -225,7 +233,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
                                   const int32_t* thr0, int32_t thr0_stride, uint32_t* bufs,
                                   uint64_t* part, int32_t* part_cnt, int32_t* out_s, int64_t* out_id, int sms,
                                   int timer_kind, cudaStream_t st, const int32_t* qfail = nullptr,
-                                  const int32_t* any = nullptr) {
+                                  const int32_t* any = nullptr, void* mscr = nullptr, size_t mscr_bytes = 0) {
   cudaEvent_t ev;
   int64_t lists = 0;
   cudaError_t e;
@@ -248,7 +256,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   const bool counted = op >= 0;
   const int32_t kin = counted ? plan_tc2(nq, n, d, k, sms, op).cap : k;
   return launch_merge_keys(part, lists, nq, kin, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr, qfail,
-                           any);
+                           any, mscr, mscr_bytes);
 }
 
 }  // namespace uq
@@ -409,13 +417,15 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     int32_t* seed_s = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
     int64_t* seed_i = reinterpret_cast<int64_t*>(ws + L.seed_i_off);
     cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, sp.rows, d, k, 0, sp.stride, nullptr, 0,
-                                   bufs, part, part_cnt, seed_s, seed_i, sms, 1, st);
+                                   bufs, part, part_cnt, seed_s, seed_i, sms, 1, st, nullptr, nullptr,
+                                   ws + L.mscr_off, L.mscr_bytes);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = seed_s + (k - 1);  // k-th best sample Delta, row stride k
   }
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
   cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, thr0_stride, bufs, part,
-                                 part_cnt, out_scores, out_ids, sms, 0, st);
+                                 part_cnt, out_scores, out_ids, sms, 0, st, nullptr, nullptr, ws + L.mscr_off,
+                                 L.mscr_bytes);
   if (e != cudaSuccess || !(sp.on && hist && need < k)) return from_cuda(e);
   // optimistic seeds: queries with fewer than k rows above their bound are
   // searched again without one (device-side flags: no host round trip; the
@@ -426,7 +436,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, nullptr, 0, bufs, part, part_cnt, out_scores,
-                     out_ids, sms, -1, st, fail, any);
+                     out_ids, sms, -1, st, fail, any, ws + L.mscr_off, L.mscr_bytes);
   return from_cuda(e);
 }
 
@@ -496,7 +506,7 @@ struct AsymLayout {
   TcPlan main;
   SeedPlan sp;
   int32_t need;
-  size_t bufs_off, part_off, cnt_off, thr_off, hist_off, qbase_off, fail_off, total;
+  size_t bufs_off, part_off, cnt_off, thr_off, hist_off, qbase_off, fail_off, mscr_off, mscr_bytes, total;
 };
 static AsymLayout asym_layout(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   AsymLayout L{};
@@ -513,7 +523,9 @@ static AsymLayout asym_layout(int64_t nq, int64_t n, int32_t d, int32_t k, int s
   L.hist_off = L.thr_off + (s ? align_up((size_t)nq * 4, 256) : 0);
   L.qbase_off = L.hist_off + (s ? align_up((size_t)nq * 256 * 4, 256) : 0);
   L.fail_off = L.qbase_off + (s ? align_up((size_t)nq * 4, 256) : 0);
-  L.total = L.fail_off + (s ? align_up((size_t)(nq + 1) * 4, 256) : 0);
+  L.mscr_off = L.fail_off + (s ? align_up((size_t)(nq + 1) * 4, 256) : 0);
+  L.mscr_bytes = merge_scratch_bytes(nq, k);
+  L.total = L.mscr_off + align_up(L.mscr_bytes, 256);
   return L;
 }
 
@@ -570,7 +582,8 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
                       q8, ldq);
   timer_end(st, ev);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
-  e = launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st, cnt);
+  e = launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st, cnt, nullptr,
+                        nullptr, ws + L.mscr_off, L.mscr_bytes);
   if (e != cudaSuccess || !(L.sp.on && L.need < k)) return from_cuda(e);
   // optimistic seeds: re-search the queries with fewer than k rows above their bound
   int32_t* fail = reinterpret_cast<int32_t*>(ws + L.fail_off);
@@ -582,7 +595,7 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
                       ldq);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   return from_cuda(launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st,
-                                     cnt, fail, any));
+                                     cnt, fail, any, ws + L.mscr_off, L.mscr_bytes));
 }
 
 uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad_rows,

@@ -23,7 +23,9 @@ cudaError_t launch_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsig
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
                               int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
                               const int32_t* counts = nullptr, const int32_t* only = nullptr,
-                              const int32_t* any = nullptr);
+                              const int32_t* any = nullptr, void* scratch = nullptr, size_t scratch_bytes = 0);
+// bytes of workspace for the two-level merge of a search with nq queries (0: single level)
+size_t merge_scratch_bytes(int64_t nq, int32_t k);
 cudaError_t launch_rerank(const void* q, uq_dtype dt, int64_t nq, int64_t ldq, const void* db, int64_t n,
                           int64_t ld, int32_t d, const int64_t* cand, int32_t n_cand, int32_t k, float* out_cos,
                           int64_t* out_ids, cudaStream_t st);

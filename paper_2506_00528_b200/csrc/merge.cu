@@ -11,6 +11,8 @@
 // bucket is taken); (2) gather the <= k keys >= T into shared memory; (3) rank
 // each selected key by counting the larger ones (keys are unique) and write
 // (score, id) at its rank, padding with (INT32_MIN, -1).
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -40,6 +42,9 @@ struct MergeParams {
   // GPUs: the merge reads every rank's [nq][k] lists directly over NVLink)
   const int32_t* const* score_ptrs;
   const int64_t* const* id_ptrs;
+  // two-level merge (few queries, many lists): CTA (q, y) merges lists
+  // [y*lpg, (y+1)*lpg) of source (a) into slot y of out_s / out_id [G][nq][k]
+  int64_t lpg;
 };
 
 template <bool FROM_SI>
@@ -71,6 +76,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q = blockIdx.x;
   if ((p.any != nullptr && *p.any == 0) || (p.only != nullptr && p.only[q] == 0)) return;
+  if (!FROM_SI && p.lpg > 0) {
+    const int64_t l0 = (int64_t)blockIdx.y * p.lpg;
+    p.lists = min(p.lpg, p.lists - l0);
+    p.keys += l0 * p.nq * p.kin;
+    if (p.counts != nullptr) p.counts += l0 * p.nq;
+    p.out_s += (size_t)blockIdx.y * p.nq * p.k;
+    p.out_id += (size_t)blockIdx.y * p.nq * p.k;
+  }
   __shared__ int s_off[kMergeMaxLists + 1];
   int64_t C = p.lists * p.kin;
   const int P = 1 << bitlen((unsigned)(p.k - 1 > 0 ? p.k - 1 : 1));  // pow2 >= k (>= 2)
@@ -217,41 +230,87 @@ static int merge_smem(int32_t k, int64_t C, int32_t* stage_cap) {
   return (int)((P + *stage_cap) * 8);
 }
 
-static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t st) {
+static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t st, unsigned groups = 1) {
   if (p.nq <= 0) return cudaSuccess;
-  const int smem = merge_smem(p.k, p.lists * p.kin, &p.stage_cap);
+  const int64_t lists_per_cta = (!from_si && p.lpg > 0) ? p.lpg : p.lists;
+  const int smem = merge_smem(p.k, lists_per_cta * p.kin, &p.stage_cap);
+  const dim3 grid((unsigned)p.nq, groups);
   if (from_si) {
     cudaError_t e = cudaFuncSetAttribute(merge_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    merge_kernel<true><<<(unsigned)p.nq, kMergeThreads, smem, st>>>(p);
+    merge_kernel<true><<<grid, kMergeThreads, smem, st>>>(p);
   } else {
     cudaError_t e = cudaFuncSetAttribute(merge_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    merge_kernel<false><<<(unsigned)p.nq, kMergeThreads, smem, st>>>(p);
+    merge_kernel<false><<<grid, kMergeThreads, smem, st>>>(p);
   }
   note_launch();
   return cudaGetLastError();
 }
 
+static int merge_sms() {
+  static const int sms = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    return v;
+  }();
+  return sms;
+}
+
+// Scratch for the two-level merge: G x nq x k (score, id) pairs, G*nq <= 2 SMs.
+size_t merge_scratch_bytes(int64_t nq, int32_t k) {
+  const int sms = merge_sms();
+  if (nq * 2 >= sms) return 0;
+  return (size_t)2 * sms * k * 12 + 1024;
+}
+
 cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, int32_t kin, int32_t k,
                               int64_t id_base, int32_t* out_s, int64_t* out_id, cudaStream_t st,
-                              const int32_t* counts, const int32_t* only, const int32_t* any) {
+                              const int32_t* counts, const int32_t* only, const int32_t* any, void* scratch,
+                              size_t scratch_bytes) {
   MergeParams p{keys, nullptr, nullptr, lists, nq, kin, k, id_base, out_s, out_id, 0, counts, only, any, nullptr,
-                nullptr};
+                nullptr, 0};
+  // Few queries over many candidate lists: one CTA per query would select
+  // among lists * kin keys alone (c2, Q = 1, k = 100, popcount engine: 44k
+  // keys, ~0.3 ms).  Split the lists over G ~ sqrt(lists) CTAs per query
+  // (G * nq <= 2 SMs), each keeping its k best, then merge the G partials.
+  const int sms = merge_sms();
+  if (scratch != nullptr && nq * 2 < sms && lists >= 8 && lists * kin > 4096) {
+    // G ~ sqrt(lists): both levels select among ~sqrt(lists) * kin keys
+    int64_t g = 1;
+    while (g * g < lists) ++g;
+    g = std::min<int64_t>(g, (2 * sms + nq - 1) / nq);
+    const int64_t lpg = (lists + g - 1) / g;
+    g = (lists + lpg - 1) / lpg;
+    if ((size_t)g * nq * k * 12 + 256 <= scratch_bytes && g > 1) {
+      int32_t* ss = reinterpret_cast<int32_t*>(scratch);
+      int64_t* si = reinterpret_cast<int64_t*>(
+          (reinterpret_cast<uintptr_t>(ss + (size_t)g * nq * k) + 255) & ~(uintptr_t)255);
+      MergeParams p1 = p;
+      p1.out_s = ss;
+      p1.out_id = si;
+      p1.lpg = lpg;
+      cudaError_t e = launch_merge_common(p1, false, st, (unsigned)g);
+      if (e != cudaSuccess) return e;
+      MergeParams p2{nullptr, ss, si, g, nq, k, k, 0, out_s, out_id, 0, nullptr, only, any, nullptr, nullptr, 0};
+      return launch_merge_common(p2, true, st);
+    }
+  }
   return launch_merge_common(p, false, st);
 }
 
 cudaError_t launch_merge_si(const int32_t* scores, const int64_t* ids, int64_t lists, int64_t nq,
                             int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
   MergeParams p{nullptr, scores, ids, lists, nq, k, k, 0, out_s, out_id, 0, nullptr, nullptr, nullptr, nullptr,
-                nullptr};
+                nullptr, 0};
   return launch_merge_common(p, true, st);
 }
 
 cudaError_t launch_merge_ptrs(const int32_t* const* score_ptrs, const int64_t* const* id_ptrs, int64_t lists,
                               int64_t nq, int32_t k, int32_t* out_s, int64_t* out_id, cudaStream_t st) {
   MergeParams p{nullptr, nullptr, nullptr, lists, nq, k, k, 0, out_s, out_id, 0, nullptr, nullptr, nullptr,
-                score_ptrs, id_ptrs};
+                score_ptrs, id_ptrs, 0};
   return launch_merge_common(p, true, st);
 }
 
