@@ -506,6 +506,34 @@ def main():
         line["recall"] = {"k": k, "recall_at_k": recall_at_k(out[1][:ns], gt_i), "queries": ns,
                           "ground_truth": "exact cosine, fp32 with TF32 off, on the float vectors "
                                           "(pinned to the fp64 oracle within 1e-5 relative in tests/test_recall.py)"}
+        # k@n (uq_rerank): search n = 4k candidates, re-rank them by
+        # cosine on the float vectors, keep k.  Untimed for the headline; the
+        # re-rank kernel is timed on its own over the whole query batch.
+        kn = min(4 * k, 1024)
+        if n_loc >= kn and n_loc * d * 4 <= (40 << 30):
+            ws_n = torch.empty(max(uq.search_workspace(nq, n_loc, d, kn, algo), 1), dtype=torch.uint8, device=dev)
+            uq.encode(u_q, x, out=qc)
+            _, cand = uq.search(qc, dbc, d, kn, id_base=0, algo=algo, workspace=ws_n)
+            del ws_n
+            u_db_f = datagen.rows(w, "db", id_base, n_loc, dev)
+            uq.rerank(u_q, u_db_f, cand, k)                       # warm-up
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 5
+            r0.record()
+            for _ in range(reps):
+                rr_cos, rr_ids = uq.rerank(u_q, u_db_f, cand, k)
+            r1.record()
+            torch.cuda.synchronize()
+            rr_ms = r0.elapsed_time(r1) / reps
+            gathered = nq * kn * d * u_db_f.element_size()
+            line["rerank"] = {"k": k, "n": kn, "recall_at_k_after_rerank":
+                              recall_at_k((rr_ids[:ns] + id_base), gt_i), "queries": ns,
+                              "kernel_ms": rr_ms, "candidates_per_s": nq * kn / (rr_ms * 1e-3),
+                              "gather_GB_per_s": gathered / (rr_ms * 1e-3) / 1e9,
+                              "note": "uq_rerank over the whole batch's n = 4k search candidates (float rows gathered "
+                                      "from HBM); recall on the same query sample as `recall`"}
+            del u_db_f
+            torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     line["paper_context"] = PAPER_CONTEXT

@@ -10,7 +10,7 @@
 // k@n (the fraction of the k true neighbours among the n candidates).
 //
 // One CTA per query: the query row is staged in SMEM as fp32, each warp scores
-// candidates (coalesced gather of the candidate row, fp32 FMA dot product and
+// candidates (16-byte gathers of the candidate row, fp32 FMA dot product and
 // squared norm, warp reduction), then a bitonic sort of 64-bit keys
 // (order-preserving cos bits << 32 | ~id) in SMEM selects the top k.  fp32
 // arithmetic: cosines agree with the fp64 oracle within 1e-5 relative (tests).
@@ -68,17 +68,53 @@ __global__ void __launch_bounds__(kRrThreads) rerank_kernel(const T* __restrict_
 #pragma unroll
   for (int w = 0; w < kRrWarps; ++w) qn2 += s_red[w];
 
-  // score the candidates: one warp per candidate row
+  // score the candidates: one warp per candidate row; rows whose length and
+  // stride are multiples of 16 B are read with 16-B loads, all of a lane's
+  // loads of a row issued before its arithmetic (one memory round trip per row)
   const int64_t* cq = cand + qi * (int64_t)n_cand;
+  constexpr int E = 16 / sizeof(T);   // elements per 16-B vector
+  const bool vec = (d % E) == 0 && (ld % E) == 0 && ((uintptr_t)db % 16) == 0;
   for (int c = warp; c < n_cand; c += kRrWarps) {
     const int64_t id = cq[c];
     if (id < 0 || id >= n) continue;   // padding from uq_search (n < k) or foreign ids
     const T* ur = db + id * ld;
     float dot = 0.f, un2 = 0.f;
-    for (int i = lane; i < d; i += 32) {
-      const float u = to_f32<T>(ur[i]);
-      dot = fmaf(s_q[i], u, dot);
-      un2 = fmaf(u, u, un2);
+    if (vec) {
+      const uint4* ur4 = reinterpret_cast<const uint4*>(ur);
+      const int nv = d / E;
+      for (int v0 = lane; v0 < nv; v0 += 32 * 4) {
+        uint4 buf[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v = v0 + 32 * j;
+          buf[j] = v < nv ? __ldg(ur4 + v) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v = v0 + 32 * j;
+          if (v < nv) {
+            const T* e = reinterpret_cast<const T*>(&buf[j]);
+            const float4* q4 = reinterpret_cast<const float4*>(s_q + v * E);   // 16-B SMEM reads
+#pragma unroll
+            for (int t4 = 0; t4 < E / 4; ++t4) {
+              const float4 qv = q4[t4];
+              const float qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float u = to_f32<T>(e[4 * t4 + t]);
+                dot = fmaf(qq[t], u, dot);
+                un2 = fmaf(u, u, un2);
+              }
+            }
+          }
+        }
+      }
+    } else {
+      for (int i = lane; i < d; i += 32) {
+        const float u = to_f32<T>(ur[i]);
+        dot = fmaf(s_q[i], u, dot);
+        un2 = fmaf(u, u, un2);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
