@@ -358,10 +358,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         if (MODE == kModeHist) return (sr / BN) * (BN * p.row_stride) + sr % BN;
         return sr * p.row_stride;
       };
-      auto load_block = [&](int tile, int kb, uint4& a, uint4& b) {
+      // this thread's DB row of a tile (nullptr past the data), computed once
+      // per tile: the per-block loads then cost no address arithmetic
+      auto row_src = [&](int tile) -> const uint8_t* {
         const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + r;
-        if (tile < ntiles && lr < rows && r < BH && !(p.dbg & 4)) {
-          const uint8_t* src = p.db + sample_row(row0 + lr) * cb;
+        if (tile < ntiles && lr < rows && r < BH && !(p.dbg & 4)) return p.db + sample_row(row0 + lr) * cb;
+        return nullptr;
+      };
+      auto load_block = [&](const uint8_t* src, int kb, uint4& a, uint4& b) {
+        if (src != nullptr) {
           a = __ldg(reinterpret_cast<const uint4*>(src) + kb);
           b = __ldg(reinterpret_cast<const uint4*>(src + pb) + kb);
         } else {
@@ -369,8 +374,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           b = a;
         }
       };
+      {
+        const uint8_t* src0 = row_src(0);
 #pragma unroll
-      for (int kb = 0; kb < NB; ++kb) load_block(0, kb, dp[kb], dn[kb]);
+        for (int kb = 0; kb < NB; ++kb) load_block(src0, kb, dp[kb], dn[kb]);
+      }
       long long t_loop = PROF_ON ? clk() : 0, t_wait = 0, t_we = 0, t_wf = 0;
       // L2 prefetch of this warp's 32 rows two tiles ahead (contiguous rows only):
       // the register ring hides one tile of latency, L2 covers the rest
@@ -391,6 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
       prefetch_rows(1);
       for (int tile = 0; tile < ntiles; ++tile) {
         prefetch_rows(tile + 2);
+        const uint8_t* nsrc = row_src(tile + 1);
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
 #pragma unroll
         for (int ks = 0; ks < NST; ++ks) {
@@ -408,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                 else
                   expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(p.dbg & 32));
               }
-              load_block(tile + 1, kb, dp[kb], dn[kb]);
+              load_block(nsrc, kb, dp[kb], dn[kb]);
             }
           }
           if (!(p.dbg & 16)) fence_proxy_async();
