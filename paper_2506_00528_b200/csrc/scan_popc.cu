@@ -25,6 +25,12 @@ namespace uq {
 constexpr int kScanWarps = 8;
 constexpr int kScanThreads = kScanWarps * 32;
 constexpr int kStageRows = kScanThreads;  // one row per thread per stage
+// stages between stream checks: up to 4, fewer for large k so that a buffer
+// (k + (check + 1) stages of keys) stays within the stream cut's 1536 keys
+static int popc_check(int32_t k) {
+  const int c = (1536 - k) / kStageRows - 1;
+  return c < 1 ? 1 : (c > 4 ? 4 : c);
+}
 
 struct PopcParams {
   const uint8_t* q;
@@ -44,6 +50,7 @@ struct PopcParams {
   const int32_t* thr0;  // optional per-query seed D_k: rows with Delta < thr0[q * thr0_stride] cannot matter
   int32_t thr0_stride;
   int64_t row_stride;   // DB row r of this scan is row r * row_stride of dbcodes
+  int32_t check;        // stages between stream checks (popc_check)
 };
 
 // OCC: resident CTAs per SM the registers are capped for.  Few-query tiles
@@ -131,15 +138,20 @@ __global__ void __launch_bounds__(kScanThreads, OCC) scan_popc_kernel(PopcParams
           if (pass) mybufs[(size_t)j * p.cap + base + __popc(bal & lanemask_lt())] = key;
         }
       }
-      __syncthreads();
-      for (int j = warp; j < nqt; j += kScanWarps) {
-        const int cnt = s_cnt[j];
-        if (cnt > p.k + kStageRows) {
-          const uint32_t thr = stream_rebuild(mybufs + (size_t)j * p.cap, cnt, p.k, lane);
-          if (lane == 0) { s_thr[j] = thr; s_cnt[j] = p.k; }
+      // streams are checked (and cut back to k) every p.check stages: the
+      // buffers hold k + (check + 1) stages of keys, and the stages in
+      // between run without CTA barriers
+      if ((s0 / kStageRows) % p.check == p.check - 1 || s0 + kStageRows >= rows) {
+        __syncthreads();
+        for (int j = warp; j < nqt; j += kScanWarps) {
+          const int cnt = s_cnt[j];
+          if (cnt > p.k + kStageRows) {
+            const uint32_t thr = stream_rebuild(mybufs + (size_t)j * p.cap, cnt, p.k, lane);
+            if (lane == 0) { s_thr[j] = thr; s_cnt[j] = p.k; }
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
     // finalize: cut each stream to k and publish its global keys
     for (int j = warp; j < nqt; j += kScanWarps) {
@@ -161,7 +173,7 @@ PopcPlan plan_popc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms) {
   const int NB = blocks128(d);
   pl.qt = (int32_t)(nq < 64 ? (nq > 0 ? nq : 1) : 64);
   pl.n_qtiles = (int32_t)((nq + pl.qt - 1) / pl.qt);
-  pl.cap = k + 2 * kStageRows;
+  pl.cap = k + (popc_check(k) + 1) * kStageRows;
   const int grid_max = sms * popc_occ(NB, pl.qt);   // resident CTAs (launch bounds)
   const KeyFmt kf = make_keyfmt(d);
   const int64_t lmax = ((int64_t)kf.rmask + 1) / kStageRows * kStageRows;
@@ -203,7 +215,7 @@ cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, in
                              const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                              cudaStream_t st) {
   PopcParams p{q, nq, db, n, d, k, make_keyfmt(d), pl.qt, pl.n_qtiles, pl.n_chunks, pl.L, pl.cap,
-               bufs, part, thr0, thr0_stride, row_stride};
+               bufs, part, thr0, thr0_stride, row_stride, popc_check(k)};
   switch (blocks128(d)) {
 #define UQ_POPC_CASE(N) \
   case N: return launch_popc_nb<N>(p, pl, st);
