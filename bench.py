@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override DB rows per GPU")
     ap.add_argument("--nq", type=int, default=None, help="override query batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-f4-index", action="store_true",
+                    help="E2M1 pair engine expands the 2-bit codes itself instead of reading the E2M1 index")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N>1: NCCL allgather + merge, or one merge kernel reading every rank's lists "
                          "from symmetric (peer-mapped) memory")
@@ -279,6 +281,12 @@ def main():
     qc = torch.empty((nq, uq.code_bytes(d)), dtype=torch.uint8, device=dev)
     out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
            torch.empty((nq, k), dtype=torch.int64, device=dev))
+    # E2M1 index (uq_build_f4_index): when the search would run on the E2M1 pair
+    # engine, its operand is expanded once at index build (outside the step,
+    # like the encode) and every scan stage is one bulk copy
+    f4x = None
+    if not args.no_f4_index and not asym and uq.search_resolve(nq, n_loc, d, k, algo) == uq.ALGO_TC_FP4:
+        f4x = uq.build_f4_index(dbc, d)
     ws_bytes = uq.search_asym_workspace(nq, n_loc, d, k) if asym else uq.search_workspace(nq, n_loc, d, k, algo)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     q8 = torch.empty((nq, d), dtype=torch.int8, device=dev)
@@ -295,7 +303,7 @@ def main():
         else:
             uq.encode(q_dev, x, out=qc)
             launches[0] += uq.last_launches()
-            s, i = uq.search(qc, dbc, d, k, id_base=id_base, algo=algo, workspace=ws, out=o)
+            s, i = uq.search(qc, dbc, d, k, id_base=id_base, algo=algo, workspace=ws, out=o, f4_index=f4x)
         launches[0] += uq.last_launches()
         if world > 1 and peer is not None:
             s, i = peer.merge(s, i)
@@ -411,6 +419,8 @@ def main():
     algo_name = "tcgen05-f4" if used_f4 else "tcgen05" if used_tc else "popc"
     if asym:
         used_f4, used_tc, algo_name = False, True, "tcgen05-asym-int8"
+    if f4x is not None:
+        algo_name = "tcgen05-f4-index"
     # dominant kernel = the main scan (every DB row); per launch: nq * n_loc Delta evaluations
     scan_avg_s = (main_ms / max(main_n, 1)) * 1e-3
     evals_per_launch = main_evals / max(main_n, 1)
@@ -423,7 +433,13 @@ def main():
                 "frac": achieved / peak, "traffic": None,
                 "kernel": "scan_tc2_kernel<NB,0,1> (CTA-pair E2M1 tcgen05 kind::mxf4 Delta GEMM + fused top-k)",
                 "peak_source": f"4 x bf16_tflops of {peaks_src} MEASURED_PEAKS.json (dense fp4 = 4x bf16 nominal)",
-                "algorithmic": "2*d ops per Delta (d E2M1 MACs)"}
+                "algorithmic": "2*d ops per Delta (d E2M1 MACs)",
+                # the rule's peak (4 x measured cuBLAS bf16) is below what UTCOMMA.2CTA
+                # sustains back to back (tools/fp4_probe.cu): both fractions reported
+                "raw_mma_peak": 8592.0,
+                "raw_mma_peak_source": "tools/fp4_probe.cu: back-to-back tcgen05.mma.cta_group::2.kind::mxf4 "
+                                       "(M=256, N=256, K=64) on all 148 SMs",
+                "frac_of_raw_mma_peak": achieved / 8592.0}
     elif used_tc:
         # int8 MACs: d per Delta (the int8 GEMM T_q . T_db^T), 2 ops per MAC
         ops = 2.0 * d * evals_per_launch
@@ -484,6 +500,10 @@ def main():
                    "l2": f"inputs larger than L2: {n_loc * uq.code_bytes(d) / 1e6:.0f} MB of DB codes per GPU scanned per step"},
         "qps": nq * args.steps / (ms * 1e-3),
         "roofline": roof,
+        "index": {"codes_bytes": n_loc * uq.code_bytes(d),
+                  "f4_index_bytes": int(f4x.numel()) if f4x is not None else 0,
+                  "note": "E2M1 operand image of the codes (4 bits per dim), built once with the index"
+                          if f4x is not None else "2-bit codes only"},
         "encode": {"rows_per_s": n_loc / (enc_ms * 1e-3), "GB_per_s": enc_bytes / (enc_ms * 1e-3) / 1e9,
                    "hbm_frac": enc_bytes / (enc_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"]),
                    "ms": enc_ms, "note": "DB index build, outside the step"},

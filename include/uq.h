@@ -129,6 +129,27 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
                        uq_stream_t stream);
 
 /*
+ * E2M1 index (an acceleration structure for UQ_ALGO_TC_FP4, not a new code
+ * format): the database codes expanded once to the E2M1 operand of the pair
+ * engine (4 bits per dim), each 120-row half tile stored as the kernel's
+ * shared-memory stage image, rows padded with zeros to whole 240-row tiles.
+ * With it a pipeline stage is one bulk copy (cp.async.bulk) instead of a
+ * 2-bit -> E2M1 expansion by the producer warps; results are identical.
+ *   uq_f4_index_bytes(n, d)                   size of the index (host call)
+ *   uq_build_f4_index(dbcodes, n, d, index)   fills it (device buffers, 16-B aligned)
+ *   uq_search_f4x(..., dbcodes, index, ...)   uq_search_ex(UQ_ALGO_TC_FP4) reading the
+ *                                             index (dbcodes still serves the
+ *                                             workspace plan; d <= 1536)
+ * Errors as uq_search_ex; UQ_ERR_UNSUPPORTED for d > 1536.
+ */
+size_t uq_f4_index_bytes(int64_t n, int32_t d);
+uq_status uq_build_f4_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_t* index,
+                            uq_stream_t stream);
+uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, const uint8_t* index,
+                        int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
+                        int64_t* out_ids, void* workspace, size_t workspace_bytes, uq_stream_t stream);
+
+/*
  * uq_merge_topk -- merge g sorted-or-unsorted candidate lists per query (e.g.
  * the per-GPU results of a sharded search after an allgather) into the k best
  * under (score desc, id asc):

@@ -18,7 +18,7 @@ __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
     "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05", "ALGO_TC_FP4",
     "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex", "rerank",
-    "quantize_i8", "search_asym", "search_asym_workspace", "merge_topk_ptrs",
+    "quantize_i8", "search_asym", "search_asym_workspace", "merge_topk_ptrs", "build_f4_index",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -55,6 +55,9 @@ def _load():
     L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
     L.uq_quantize_i8.argtypes = [vp, i32, i64, i32, i64, vp, i64, vp]
     L.uq_merge_topk_ptrs.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
+    L.uq_f4_index_bytes.argtypes, L.uq_f4_index_bytes.restype = [i64, i32], sz
+    L.uq_build_f4_index.argtypes = [vp, i64, i32, vp, vp]
+    L.uq_search_f4x.argtypes = [vp, i64, vp, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_asym_workspace.argtypes = [i64, i64, i32, i32, ctypes.POINTER(sz)]
     L.uq_search_asym.argtypes = [vp, i64, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
@@ -64,7 +67,7 @@ def _load():
                                        ctypes.POINTER(ctypes.c_double)]
     for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_timing_collect_ex", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
               "uq_check_codes", "uq_rerank", "uq_quantize_i8", "uq_search_asym_workspace", "uq_search_asym",
-              "uq_merge_topk_ptrs"):
+              "uq_merge_topk_ptrs", "uq_build_f4_index", "uq_search_f4x"):
         getattr(L, f).restype = i32
     return L
 
@@ -174,21 +177,37 @@ def search_resolve(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> in
     return int(r.value)
 
 
+def build_f4_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
+    """E2M1 index of the database codes for the pair engine (uq_build_f4_index)."""
+    _dev(dbcodes, "dbcodes")
+    n = dbcodes.shape[0]
+    out = torch.empty(max(int(_L.uq_f4_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
+    _check("uq_build_f4_index", _L.uq_build_f4_index(_ptr(dbcodes), n, d, _ptr(out), _stream(stream)))
+    return out
+
+
 def search(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base: int = 0,
            algo: int = ALGO_AUTO, workspace: Optional[torch.Tensor] = None,
            out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
-           stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+           stream=None, f4_index: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, torch.Tensor]:
     """Exhaustive proxy-space kNN (uq_search): (scores [nq][k] int32, ids [nq][k] int64),
-    best first under (Delta desc, id asc)."""
+    best first under (Delta desc, id asc).  With ``f4_index`` (build_f4_index) the E2M1
+    pair engine reads the pre-expanded index (uq_search_f4x)."""
     _dev(qcodes, "qcodes"); _dev(dbcodes, "dbcodes")
     nq, n = qcodes.shape[0], dbcodes.shape[0]
     dev = qcodes.device
     if out is None:
         out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
                torch.empty((nq, k), dtype=torch.int64, device=dev))
-    need = search_workspace(nq, n, d, k, algo)
+    need = search_workspace(nq, n, d, k, ALGO_TC_FP4 if f4_index is not None else algo)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    if f4_index is not None:
+        _dev(f4_index, "f4_index")
+        _check("uq_search_f4x", _L.uq_search_f4x(_ptr(qcodes), nq, _ptr(dbcodes), _ptr(f4_index), n, d, k, id_base,
+                                                 _ptr(out[0]), _ptr(out[1]), _ptr(workspace), workspace.numel(),
+                                                 _stream(stream)))
+        return out
     _check("uq_search", _L.uq_search_ex(_ptr(qcodes), nq, _ptr(dbcodes), n, d, k, id_base,
                                         _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
                                         workspace.numel(), algo, _stream(stream)))

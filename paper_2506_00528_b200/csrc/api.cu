@@ -233,7 +233,8 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
                                   const int32_t* thr0, int32_t thr0_stride, uint32_t* bufs,
                                   uint64_t* part, int32_t* part_cnt, int32_t* out_s, int64_t* out_id, int sms,
                                   int timer_kind, cudaStream_t st, const int32_t* qfail = nullptr,
-                                  const int32_t* any = nullptr, void* mscr = nullptr, size_t mscr_bytes = 0) {
+                                  const int32_t* any = nullptr, void* mscr = nullptr, size_t mscr_bytes = 0,
+                                  const uint8_t* dbx = nullptr) {
   cudaEvent_t ev;
   int64_t lists = 0;
   cudaError_t e;
@@ -242,7 +243,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   if (is_tc(a)) {
     const TcPlan tp = plan_tc_for(a, nq, n, d, k, sms);
     e = op >= 0 ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, op, st,
-                                  qfail, any)
+                                  qfail, any, nullptr, 0, dbx)
                 : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
     lists = tp.n_chunks;
   } else {
@@ -371,9 +372,10 @@ uq_status uq_search_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_
   return uq_search_workspace_ex(nq, n, d, k, UQ_ALGO_AUTO, bytes);
 }
 
-uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,
-                       int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
-                       void* workspace, size_t workspace_bytes, uq_algo algo, uq_stream_t stream) {
+static uq_status search_impl(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                             int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
+                             void* workspace, size_t workspace_bytes, uq_algo algo, uq_stream_t stream,
+                             const uint8_t* dbx) {
   g_launches = 0;
   uq_status s = validate_search(qcodes, nq, dbcodes, n, d, k);
   if (s != UQ_OK) return s;
@@ -408,7 +410,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)sp.rows);
     cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, need, sp.stride, ghist, qbase, thr,
-                                         sms, pair_op(a, nq, d), st);
+                                         sms, pair_op(a, nq, d), st, nullptr, 0, dbx);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = thr;
@@ -425,7 +427,7 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
   cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, thr0_stride, bufs, part,
                                  part_cnt, out_scores, out_ids, sms, 0, st, nullptr, nullptr, ws + L.mscr_off,
-                                 L.mscr_bytes);
+                                 L.mscr_bytes, dbx);
   if (e != cudaSuccess || !(sp.on && hist && need < k)) return from_cuda(e);
   // optimistic seeds: queries with fewer than k rows above their bound are
   // searched again without one (device-side flags: no host round trip; the
@@ -436,8 +438,37 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
   e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, nullptr, 0, bufs, part, part_cnt, out_scores,
-                     out_ids, sms, -1, st, fail, any, ws + L.mscr_off, L.mscr_bytes);
+                     out_ids, sms, -1, st, fail, any, ws + L.mscr_off, L.mscr_bytes, dbx);
   return from_cuda(e);
+}
+
+uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                       int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
+                       void* workspace, size_t workspace_bytes, uq_algo algo, uq_stream_t stream) {
+  return search_impl(qcodes, nq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace, workspace_bytes, algo,
+                     stream, nullptr);
+}
+
+size_t uq_f4_index_bytes(int64_t n, int32_t d) {
+  if (n < 0 || d < 1 || d > UQ_MAX_D) return 0;
+  return f4_index_bytes(n, d);
+}
+
+uq_status uq_build_f4_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_t* index, uq_stream_t stream) {
+  g_launches = 0;
+  if (n < 0 || d < 1) return UQ_ERR_INVALID_ARG;
+  if (blocks128(d) > 12) return UQ_ERR_UNSUPPORTED;
+  if (n == 0) return UQ_OK;
+  if (!dbcodes || !index || !aligned16(dbcodes) || !aligned16(index)) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_build_f4_index(dbcodes, n, d, index, (cudaStream_t)stream));
+}
+
+uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, const uint8_t* index, int64_t n,
+                        int32_t d, int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
+                        void* workspace, size_t workspace_bytes, uq_stream_t stream) {
+  if (index == nullptr || !aligned16(index)) return UQ_ERR_INVALID_ARG;
+  return search_impl(qcodes, nq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace, workspace_bytes,
+                     UQ_ALGO_TC_FP4, stream, index);
 }
 
 uq_status uq_search(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, int64_t n, int32_t d,

@@ -130,6 +130,7 @@ struct Params {
   const int32_t* any_fail;  // optional: the launch is a no-op unless *any_fail
   const int8_t* q8;     // optional (int8 engine): int8 queries [nq][ldq8] instead of ternary codes
   int64_t ldq8;
+  const uint8_t* dbx;   // optional (E2M1 engine): pre-expanded index (uq_build_f4_index), stages by bulk copy
   int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads,
                         // 8 cycle accounting, 16 no producer proxy fence
 };
@@ -227,7 +228,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
   uint64_t* empty = bars + p.stages;       // [stages] (each CTA): MMA commit
   uint64_t* tfull = bars + 2 * p.stages;   // [2] (each CTA): MMA commit
   uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps per set
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* loaded = tempty + 2;           // [stages] (each CTA): bulk-copy transaction barriers (dbx mode)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(loaded + p.stages);
+  const bool xmode = OP == kOpF4 && p.dbx != nullptr;
 
   // seed fallback pass with nothing to redo: every thread of both CTAs leaves
   if (p.any_fail != nullptr && *p.any_fail == 0) return;
@@ -241,8 +244,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), 2 * kProdWarps);
+      mbar_init(smem_u32(&full[s]), xmode ? 2 : 2 * kProdWarps);   // dbx: one forwarder per CTA
       mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&loaded[s]), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
@@ -339,7 +343,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
     fence_proxy_async();
     cluster_sync();  // both CTAs' A tiles are in place before the leader issues
 
-    if (warp < kProdWarps) {
+    if (warp < kProdWarps && xmode) {
+      // ======= pre-expanded index: a stage is one bulk copy of its SMEM image =======
+      // The index stores each 120-row half tile as the K-major stage layout of
+      // this kernel (block kb, chunk c, row group, row: uq_build_f4_index), so
+      // the bytes of blocks [ks*bps, ks*bps+bps) of a half tile are contiguous.
+      // Warp 0 lane 0 issues the copies (transaction-counted on loaded[stage]),
+      // warp 1 lane 0 forwards their completion to the pair's full barrier,
+      // warp 3 of the leader issues the MMAs.
+      const uint32_t full_dst = mapa(smem_u32(&full[0]), 0);
+      constexpr uint32_t kHalfTileBytes = (uint32_t)NB * G::CPB * BH * 16;
+      auto half_tile = [&](int tile) -> int64_t {   // global 120-row half-tile index of (tile, this CTA)
+        const int64_t sr = (int64_t)tile * BN + (int64_t)cr * BH;
+        const int64_t row = MODE == kModeHist ? (sr / BN) * (BN * p.row_stride) + sr % BN : sr * p.row_stride;
+        return (row0 + row) / BH;   // row0 and BN-row blocks are multiples of BH
+      };
+      if (warp == 0 && lane == 0) {
+        for (int tile = 0; tile < ntiles; ++tile) {
+          const uint8_t* img = p.dbx + (size_t)half_tile(tile) * kHalfTileBytes;
+          for (int ks = 0; ks < NST; ++ks) {
+            const int nb = (ks + 1) * kBlkPerStage <= NB ? kBlkPerStage : NB - ks * kBlkPerStage;
+            const uint32_t bytes = (uint32_t)nb * G::CPB * BH * 16;
+            mbar_wait(smem_u32(&empty[stage]), sphase ^ 1u);
+            const uint32_t bar = smem_u32(&loaded[stage]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sB + (size_t)stage * kStageBytes)),
+                "l"(img + (size_t)ks * kBlkPerStage * G::CPB * BH * 16), "r"(bytes), "r"(bar)
+                : "memory");
+            if (++stage == S) { stage = 0; sphase ^= 1u; }
+          }
+        }
+      } else if (warp == 1 && lane == 0) {
+        for (int tile = 0; tile < ntiles; ++tile)
+          for (int ks = 0; ks < NST; ++ks) {
+            mbar_wait(smem_u32(&loaded[stage]), sphase);
+            mbar_arrive_cluster(full_dst + (uint32_t)stage * 8u);
+            if (++stage == S) { stage = 0; sphase ^= 1u; }
+          }
+      } else if (leader && warp == kMmaWarp) {
+        constexpr uint32_t idesc = idesc_mxf4(2 * BM, BN);
+        const uint32_t sf_tmem = tmem_base + G::SF_COL;
+        const uint64_t a_desc0 = smem_desc(smem_u32(sA), A_LBO, SBO);
+        const uint64_t b_desc0 = smem_desc(smem_u32(sB), B_LBO, SBO);
+        for (int tile = 0; tile < ntiles; ++tile) {
+          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
+          for (int ks = 0; ks < NST; ++ks) {
+            if (ks == 0) mbar_wait_cluster(smem_u32(&tempty[acc]), aphase ^ 1u);
+            mbar_wait_cluster(smem_u32(&full[stage]), sphase);
+            tc_fence_after();
+            const uint64_t b_stage = b_desc0 + (uint64_t)(((uint32_t)stage * kStageBytes) >> 4);
+            if (elect_one()) {
+#pragma unroll
+              for (int bb = 0; bb < kBlkPerStage; ++bb) {
+                const int kb = ks * kBlkPerStage + bb;
+                if (kb < NB) {
+#pragma unroll
+                  for (int kk = 0; kk < G::MPB; ++kk) {
+                    const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)(kb * G::CPB + kk * 2) * A_LBO) >> 4);
+                    const uint64_t bd = b_stage + (uint64_t)(((uint32_t)(bb * G::CPB + kk * 2) * B_LBO) >> 4);
+                    mma2_f4(d_tmem, ad, bd, idesc, sf_tmem, sf_tmem, (kb | kk) != 0 ? 1u : 0u);
+                  }
+                }
+              }
+              mma2_commit_mc(smem_u32(&empty[stage]), 0x3);
+              if (ks == NST - 1) mma2_commit_mc(smem_u32(&tfull[acc]), 0x3);
+            }
+            __syncwarp();
+            if (++stage == S) { stage = 0; sphase ^= 1u; }
+          }
+          if (++acc == 2) { acc = 0; aphase ^= 1u; }
+        }
+      }
+    } else if (warp < kProdWarps) {
       // ================= producers: rows [cr*BH, cr*BH+BH) of each tile =================
       // Warp kMmaWarp of the leader CTA is also the MMA issuer: after writing
       // its rows of a stage it waits for the pair's `full` barrier and issues
@@ -811,6 +888,54 @@ __global__ void thr_from_hist_kernel(uint32_t* ghist, int64_t nq, int32_t k, con
   }
 }
 
+// E2M1 index: every 120-row half tile stored as the pair kernel's K-major
+// stage image -- [NB blocks][4 chunks][15 row groups][8 rows][16 B], chunk c of
+// block kb = expand_word_f4 of plane word 4 kb + c -- rows padded with zeros to
+// whole 240-row pair tiles.  One thread per (row, block).
+__global__ void build_f4_index_kernel(const uint8_t* __restrict__ codes, int64_t n, int64_t n_pad, int NB,
+                                      uint8_t* __restrict__ index) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pad * NB) return;
+  const int64_t r = t / NB;
+  const int kb = (int)(t % NB);
+  const int64_t pb = (int64_t)NB * 16;
+  uint4 pw = make_uint4(0, 0, 0, 0), nw = pw;
+  if (r < n) {
+    pw = *reinterpret_cast<const uint4*>(codes + r * 2 * pb + kb * 16);
+    nw = *reinterpret_cast<const uint4*>(codes + r * 2 * pb + pb + kb * 16);
+  }
+  const uint32_t pp[4] = {pw.x, pw.y, pw.z, pw.w}, nn[4] = {nw.x, nw.y, nw.z, nw.w};
+  constexpr int HT = 120;
+  const int64_t h = r / HT;
+  const int j = (int)(r % HT);
+  uint8_t* base = index + (size_t)h * NB * 4 * HT * 16 + (size_t)kb * 4 * HT * 16 + (j >> 3) * 128 + (j & 7) * 16;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t o[4];
+    ::uq::tc::expand_word_f4(pp[c], nn[c], o);
+    *reinterpret_cast<uint4*>(base + (size_t)c * HT * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+}  // namespace tc2
+
+size_t f4_index_bytes(int64_t n, int32_t d) {
+  const int64_t n_pad = (n + 239) / 240 * 240;
+  return (size_t)n_pad * blocks128(d) * 64;
+}
+
+cudaError_t launch_build_f4_index(const uint8_t* codes, int64_t n, int32_t d, uint8_t* index, cudaStream_t st) {
+  const int NB = blocks128(d);
+  const int64_t n_pad = (n + 239) / 240 * 240;
+  const int64_t threads = n_pad * NB;
+  if (threads == 0) return cudaSuccess;
+  tc2::build_f4_index_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(codes, n, n_pad, NB, index);
+  note_launch();
+  return cudaGetLastError();
+}
+
+namespace tc2 {
+
 // fail[q] = the query was filtered by a seed and its k-th result is padding
 // (fewer than k rows passed the optimistic bound): it must be searched again
 __global__ void seed_verify_kernel(const int64_t* out_ids, int64_t nq, int32_t k, const int32_t* thr, int32_t* fail,
@@ -893,7 +1018,7 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
   const int64_t pairs = pl.n_items < npairs ? pl.n_items : npairs;
   pl.grid = (int32_t)(2 * pairs);
   pl.smem = 1024 + tc2::BM * NB * G::RB + pl.stages * G::stage_bytes(NB) +
-            (mode == tc2::kModeHist ? tc2::hist_bytes(OP, NB) : 0) + (2 * pl.stages + 4) * 8 + 16;
+            (mode == tc2::kModeHist ? tc2::hist_bytes(OP, NB) : 0) + (3 * pl.stages + 4) * 8 + 16;
   pl.buf_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.grid * G::sets(mode) * tc2::BM * pl.cap * 4;
   pl.part_bytes = (mode == tc2::kModeHist) ? 0 : (size_t)pl.n_chunks * nq * pl.cap * 8;
   return pl;
@@ -973,11 +1098,12 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st, const int32_t* qfail, const int32_t* any_fail, const int8_t* q8,
-                            int64_t ldq8) {
+                            int64_t ldq8, const uint8_t* dbx) {
+  if (dbx != nullptr && op != tc2::kOpF4) return cudaErrorInvalidValue;
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(q8 ? 127 * d : d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
-                thr0_stride, row_stride, nullptr, 0.f, nullptr, 0.f, qfail, any_fail, q8, ldq8, tc2_dbg()};
+                thr0_stride, row_stride, nullptr, 0.f, nullptr, 0.f, qfail, any_fail, q8, ldq8, dbx, tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
 
@@ -986,7 +1112,9 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
 // (left zero on exit).
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
-                                 int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8, int64_t ldq8) {
+                                 int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8, int64_t ldq8,
+                                 const uint8_t* dbx) {
+  if (dbx != nullptr && op != tc2::kOpF4) return cudaErrorInvalidValue;
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;
@@ -1002,7 +1130,7 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
-                nullptr, 0, row_stride, ghist, z, qbase, topsig, nullptr, nullptr, q8, ldq8, tc2_dbg()};
+                nullptr, 0, row_stride, ghist, z, qbase, topsig, nullptr, nullptr, q8, ldq8, dbx, tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, need, qbase, thr);

@@ -60,6 +60,15 @@ def test_fuzz_engines(uq, orc, seed):
         assert np.array_equal(i.cpu().numpy(), i_ref), (seed, algo, d, x, n, nq, k, mode)
         ran += 1
     assert ran >= 1
+    try:
+        uq.search_workspace(nq, n, d, k, uq.ALGO_TC_FP4)
+        f4_ok = n > 0
+    except uq.UQError:
+        f4_ok = False
+    if f4_ok:   # the E2M1 engine fed by the pre-expanded index
+        s, i = uq.search(qg, dbg, d, k, id_base=11, f4_index=uq.build_f4_index(dbg, d))
+        assert np.array_equal(s.cpu().numpy(), s_ref), (seed, "f4x", d, x, n, nq, k, mode)
+        assert np.array_equal(i.cpu().numpy(), i_ref), (seed, "f4x", d, x, n, nq, k, mode)
     if d <= 1024:
         q8 = orc.quantize_i8(u_q)
         s, i = uq.search_asym(torch.from_numpy(q8).cuda(), dbg, d, k, id_base=11)

@@ -497,3 +497,27 @@ def test_peer_exchange_world1(uq):
         if owned:
             torch.cuda.synchronize()
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,x,n,nq,k,mode", [(384, 192, 5000, 130, 10, "normal"), (768, 384, 20001, 300, 100, "dup"),
+                                             (1024, 512, 131072, 260, 10, "normal"), (1536, 768, 70001, 140, 100, "dup"),
+                                             (129, 40, 241, 3, 7, "ties"), (128, 64, 100000, 600, 1, "ties")])
+def test_search_f4_index_parity(uq, orc, d, x, n, nq, k, mode):
+    """E2M1 pair engine fed by the pre-expanded index (bulk-copy stages) equals
+    the oracle, including seeded scans (n >= 2^16) and ragged tails."""
+    rng = np.random.default_rng(d + n)
+    if mode == "dup":
+        base = rng.standard_normal((max(1, n // 7), d)).astype(np.float32)
+        u_db = base[rng.integers(0, base.shape[0], size=n)]
+    elif mode == "ties":
+        u_db = _tie_heavy(rng, n, d)
+    else:
+        u_db = rng.standard_normal((n, d)).astype(np.float32)
+    u_q = rng.standard_normal((nq, d)).astype(np.float32)
+    o_db = orc.pack(orc.encode(u_db, x))
+    o_q = orc.pack(orc.encode(u_q, x))
+    dbc = torch.from_numpy(o_db).cuda()
+    idx = uq.build_f4_index(dbc, d)
+    s, i = uq.search(torch.from_numpy(o_q).cuda(), dbc, d, k, id_base=3, f4_index=idx)
+    s_ref, i_ref = orc.knn(o_q, o_db, d, k, id_base=3)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
