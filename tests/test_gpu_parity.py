@@ -521,3 +521,18 @@ def test_search_f4_index_parity(uq, orc, d, x, n, nq, k, mode):
     s, i = uq.search(torch.from_numpy(o_q).cuda(), dbc, d, k, id_base=3, f4_index=idx)
     s_ref, i_ref = orc.knn(o_q, o_db, d, k, id_base=3)
     assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
+
+
+@pytest.mark.parametrize("opt,k", [("0.01", 500), ("0", 100)])
+def test_search_f4_index_seed_fallback(uq, orc, monkeypatch, opt, k):
+    """Index-fed E2M1 engine with forced seed fallbacks (and exact seeds)."""
+    monkeypatch.setenv("UQ_SEED_OPT", opt)
+    rng = np.random.default_rng(40 + k)
+    d, x, n, nq = 256, 128, 131072, 300
+    u_db = rng.standard_normal((n, d)).astype(np.float32)
+    u_q = rng.standard_normal((nq, d)).astype(np.float32)
+    o_db, o_q = orc.pack(orc.encode(u_db, x)), orc.pack(orc.encode(u_q, x))
+    dbc = torch.from_numpy(o_db).cuda()
+    s, i = uq.search(torch.from_numpy(o_q).cuda(), dbc, d, k, f4_index=uq.build_f4_index(dbc, d))
+    s_ref, i_ref = orc.knn(o_q, o_db, d, k)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
