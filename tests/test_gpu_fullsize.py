@@ -57,6 +57,13 @@ def _check_chunks(uq, orc, w, x, dbc, rng, nchunks=2):
         assert np.array_equal(got, ref), (w.name, x, c)
 
 
+def _check_index_path(uq, qc, dbc, d, k, s, i):
+    """The bench's launch configuration for the E2M1 engine reads the E2M1 index:
+    its full result must equal the 2-bit path's byte for byte (all queries)."""
+    s2, i2 = uq.search(qc, dbc, d, k, f4_index=uq.build_f4_index(dbc, d))
+    assert torch.equal(s2, s) and torch.equal(i2, i)
+
+
 def _check_queries(uq, orc, w, x, qc_gpu, s_gpu, i_gpu, dbc, rng, nsample):
     qs = np.sort(rng.choice(w.nq, size=nsample, replace=False))
     q = datagen.queries(w, "cuda").cpu().numpy()[qs]
@@ -80,6 +87,7 @@ def test_full_size_c3_sampled(uq, orc):
         qc = uq.encode(qf, x)
         s, i = uq.search(qc, dbc, w.d, w.k)
         _check_queries(uq, orc, w, x, qc, s, i, dbc, rng, nsample=6)
+        _check_index_path(uq, qc, dbc, w.d, w.k, s, i)
 
 
 def test_full_size_c5_sampled(uq, orc):
@@ -94,6 +102,7 @@ def test_full_size_c5_sampled(uq, orc):
     # Q = 1 (the HBM-bound case) and Q = 1024
     s1, i1 = uq.search(qc_all[:1], dbc, w.d, w.k)
     s, i = uq.search(qc_all, dbc, w.d, w.k)
+    _check_index_path(uq, qc_all, dbc, w.d, w.k, s, i)
     db_h = dbc.cpu().numpy()
     qs = np.concatenate([[0], np.sort(rng.choice(np.arange(1, w.nq), size=3, replace=False))])
     o_q = orc.pack(orc.encode(qf.cpu().numpy()[qs], w.x))
@@ -126,6 +135,8 @@ def test_full_size_c4_shard_sampled(uq, orc):
     qf = datagen.queries(w, "cuda")
     qc = uq.encode(qf, w.x)
     s, i = uq.search(qc, dbc, w.d, w.k, id_base=lo)
+    s2, i2 = uq.search(qc, dbc, w.d, w.k, id_base=lo, f4_index=uq.build_f4_index(dbc, w.d))
+    assert torch.equal(s2, s) and torch.equal(i2, i)   # the bench's index-fed launch, all queries
     qs = np.sort(rng.choice(w.nq, size=3, replace=False))
     o_q = orc.pack(orc.encode(qf.cpu().numpy()[qs], w.x))
     assert np.array_equal(qc.cpu().numpy()[qs], o_q)

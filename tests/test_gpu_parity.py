@@ -235,7 +235,10 @@ def test_full_size_c2_sampled(uq, orc):
     db = datagen.db(w, "cuda")
     q = datagen.queries(w, "cuda")
     dbc, qc = uq.encode(db, w.x), uq.encode(q, w.x)
-    s, i = uq.search(qc, dbc, w.d, w.k)              # whole batch, as bench.py runs it
+    s, i = uq.search(qc, dbc, w.d, w.k)              # whole batch, AUTO engine
+    # bench.py's launch: the E2M1 engine reading the E2M1 index -- all queries equal
+    s2, i2 = uq.search(qc, dbc, w.d, w.k, f4_index=uq.build_f4_index(dbc, w.d))
+    assert torch.equal(s2, s) and torch.equal(i2, i)
     db_h = db.cpu().numpy()
     del db
     o_db = orc.pack(orc.encode(db_h, w.x))
