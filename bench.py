@@ -284,6 +284,7 @@ def main():
     # E2M1 index (uq_build_f4_index): when the search would run on the E2M1 pair
     # engine, its operand is expanded once at index build (outside the step,
     # like the encode) and every scan stage is one bulk copy
+    i8x = uq.build_i8_index(dbc, d) if (asym and not args.no_f4_index and d <= 1024) else None
     f4x = None
     if not args.no_f4_index and not asym and uq.search_resolve(nq, n_loc, d, k, algo) == uq.ALGO_TC_FP4:
         f4x = uq.build_f4_index(dbc, d)
@@ -299,7 +300,7 @@ def main():
         if asym:   # quantise the float queries to int8, masked-addition search
             uq.quantize_i8(q_dev, out=q8)
             launches[0] += uq.last_launches()
-            s, i = uq.search_asym(q8, dbc, d, k, id_base=id_base, workspace=ws, out=o)
+            s, i = uq.search_asym(q8, dbc, d, k, id_base=id_base, workspace=ws, out=o, i8_index=i8x)
         else:
             uq.encode(q_dev, x, out=qc)
             launches[0] += uq.last_launches()
@@ -502,6 +503,7 @@ def main():
         "roofline": roof,
         "index": {"codes_bytes": n_loc * uq.code_bytes(d),
                   "f4_index_bytes": int(f4x.numel()) if f4x is not None else 0,
+                  "i8_index_bytes": int(i8x.numel()) if i8x is not None else 0,
                   "note": "E2M1 operand image of the codes (4 bits per dim), built once with the index"
                           if f4x is not None else "2-bit codes only"},
         "encode": {"rows_per_s": n_loc / (enc_ms * 1e-3), "GB_per_s": enc_bytes / (enc_ms * 1e-3) / 1e9,

@@ -150,6 +150,21 @@ uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcode
                         int64_t* out_ids, void* workspace, size_t workspace_bytes, uq_stream_t stream);
 
 /*
+ * int8 index: the same acceleration structure for the int8 pair engine (8
+ * bits per dim, 128-row half tiles as its stage image, rows padded to 256),
+ * used by single-operand search.  d <= 1024.
+ *   uq_i8_index_bytes(n, d), uq_build_i8_index(dbcodes, n, d, index)
+ *   uq_search_asym_x(...)   uq_search_asym reading the index
+ */
+size_t uq_i8_index_bytes(int64_t n, int32_t d);
+uq_status uq_build_i8_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_t* index,
+                            uq_stream_t stream);
+uq_status uq_search_asym_x(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes,
+                           const uint8_t* index, int64_t n, int32_t d, int32_t k, int64_t id_base,
+                           int32_t* out_scores, int64_t* out_ids, void* workspace,
+                           size_t workspace_bytes, uq_stream_t stream);
+
+/*
  * uq_merge_topk -- merge g sorted-or-unsorted candidate lists per query (e.g.
  * the per-GPU results of a sharded search after an allgather) into the k best
  * under (score desc, id asc):

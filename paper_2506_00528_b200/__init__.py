@@ -18,7 +18,7 @@ __all__ = [
     "UQError", "lib_path", "code_bytes", "plane_bytes", "encode", "scores", "search",
     "search_workspace", "search_resolve", "merge_topk", "check_codes", "ALGO_AUTO", "ALGO_POPC", "ALGO_TCGEN05", "ALGO_TC_FP4",
     "last_launches", "version", "timing_enable", "timing_collect", "timing_collect_ex", "rerank",
-    "quantize_i8", "search_asym", "search_asym_workspace", "merge_topk_ptrs", "build_f4_index",
+    "quantize_i8", "search_asym", "search_asym_workspace", "merge_topk_ptrs", "build_f4_index", "build_i8_index",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -58,6 +58,9 @@ def _load():
     L.uq_f4_index_bytes.argtypes, L.uq_f4_index_bytes.restype = [i64, i32], sz
     L.uq_build_f4_index.argtypes = [vp, i64, i32, vp, vp]
     L.uq_search_f4x.argtypes = [vp, i64, vp, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
+    L.uq_i8_index_bytes.argtypes, L.uq_i8_index_bytes.restype = [i64, i32], sz
+    L.uq_build_i8_index.argtypes = [vp, i64, i32, vp, vp]
+    L.uq_search_asym_x.argtypes = [vp, i64, i64, vp, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_asym_workspace.argtypes = [i64, i64, i32, i32, ctypes.POINTER(sz)]
     L.uq_search_asym.argtypes = [vp, i64, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
@@ -67,7 +70,8 @@ def _load():
                                        ctypes.POINTER(ctypes.c_double)]
     for f in ("uq_search_resolve", "uq_timing_enable", "uq_timing_collect", "uq_timing_collect_ex", "uq_encode", "uq_scores", "uq_search_workspace_ex", "uq_search_ex", "uq_merge_topk",
               "uq_check_codes", "uq_rerank", "uq_quantize_i8", "uq_search_asym_workspace", "uq_search_asym",
-              "uq_merge_topk_ptrs", "uq_build_f4_index", "uq_search_f4x"):
+              "uq_merge_topk_ptrs", "uq_build_f4_index", "uq_search_f4x", "uq_build_i8_index",
+              "uq_search_asym_x"):
         getattr(L, f).restype = i32
     return L
 
@@ -186,6 +190,15 @@ def build_f4_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
     return out
 
 
+def build_i8_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
+    """int8 index of the database codes for single-operand search (uq_build_i8_index)."""
+    _dev(dbcodes, "dbcodes")
+    n = dbcodes.shape[0]
+    out = torch.empty(max(int(_L.uq_i8_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
+    _check("uq_build_i8_index", _L.uq_build_i8_index(_ptr(dbcodes), n, d, _ptr(out), _stream(stream)))
+    return out
+
+
 def search(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base: int = 0,
            algo: int = ALGO_AUTO, workspace: Optional[torch.Tensor] = None,
            out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
@@ -237,7 +250,7 @@ def search_asym_workspace(nq: int, n: int, d: int, k: int) -> int:
 def search_asym(q8: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base: int = 0,
                 workspace: Optional[torch.Tensor] = None,
                 out: Optional[Tuple[torch.Tensor, torch.Tensor]] = None,
-                stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
+                stream=None, i8_index: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, torch.Tensor]:
     """Single-operand kNN (uq_search_asym): int8 queries q8 [nq][d]
     against ternary codes by masked addition; (scores int32, ids int64) [nq][k]."""
     _dev(q8, "q8"); _dev(dbcodes, "dbcodes")
@@ -251,6 +264,12 @@ def search_asym(q8: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base
     need = search_asym_workspace(nq, n, d, k)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    if i8_index is not None:
+        _dev(i8_index, "i8_index")
+        _check("uq_search_asym_x", _L.uq_search_asym_x(_ptr(q8), nq, q8.stride(0), _ptr(dbcodes), _ptr(i8_index), n,
+                                                       d, k, id_base, _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
+                                                       workspace.numel(), _stream(stream)))
+        return out
     _check("uq_search_asym", _L.uq_search_asym(_ptr(q8), nq, q8.stride(0), _ptr(dbcodes), n, d, k, id_base,
                                                _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
                                                workspace.numel(), _stream(stream)))

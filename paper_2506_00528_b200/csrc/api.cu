@@ -571,9 +571,9 @@ uq_status uq_search_asym_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, 
   return UQ_OK;
 }
 
-uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, int64_t n, int32_t d,
-                         int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids, void* workspace,
-                         size_t workspace_bytes, uq_stream_t stream) {
+static uq_status asym_impl(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                           int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids, void* workspace,
+                           size_t workspace_bytes, uq_stream_t stream, const uint8_t* dbx) {
   g_launches = 0;
   if (nq < 0 || n < 0 || d < 1 || k < 1 || ldq < d) return UQ_ERR_INVALID_ARG;
   if ((nq > 0 && q8 == nullptr) || (n > 0 && nq > 0 && dbcodes == nullptr)) return UQ_ERR_INVALID_ARG;
@@ -602,7 +602,7 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)L.sp.rows);
     e = launch_seed_tc2_hist(nullptr, nq, dbcodes, L.sp.rows, d, k, L.need, L.sp.stride, ghist, qbase, thr, sms, 0,
-                             st, q8, ldq);
+                             st, q8, ldq, dbx);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = thr;
@@ -610,7 +610,7 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
   cudaEvent_t ev;
   timer_begin(st, &ev, 0, (double)nq * (double)n);
   e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, thr0, 1, 1, 0, st, nullptr, nullptr,
-                      q8, ldq);
+                      q8, ldq, dbx);
   timer_end(st, ev);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st, cnt, nullptr,
@@ -623,10 +623,39 @@ uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_
   e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, nullptr, 0, 1, 0, st, fail, any, q8,
-                      ldq);
+                      ldq, dbx);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   return from_cuda(launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st,
                                      cnt, fail, any, ws + L.mscr_off, L.mscr_bytes));
+}
+
+uq_status uq_search_asym(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, int64_t n, int32_t d,
+                         int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids, void* workspace,
+                         size_t workspace_bytes, uq_stream_t stream) {
+  return asym_impl(q8, nq, ldq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace, workspace_bytes, stream,
+                   nullptr);
+}
+
+size_t uq_i8_index_bytes(int64_t n, int32_t d) {
+  if (n < 0 || d < 1 || d > UQ_MAX_D) return 0;
+  return i8_index_bytes(n, d);
+}
+
+uq_status uq_build_i8_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_t* index, uq_stream_t stream) {
+  g_launches = 0;
+  if (n < 0 || d < 1) return UQ_ERR_INVALID_ARG;
+  if (blocks128(d) > 8) return UQ_ERR_UNSUPPORTED;
+  if (n == 0) return UQ_OK;
+  if (!dbcodes || !index || !aligned16(dbcodes) || !aligned16(index)) return UQ_ERR_INVALID_ARG;
+  return from_cuda(launch_build_i8_index(dbcodes, n, d, index, (cudaStream_t)stream));
+}
+
+uq_status uq_search_asym_x(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, const uint8_t* index,
+                           int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
+                           void* workspace, size_t workspace_bytes, uq_stream_t stream) {
+  if (index == nullptr || !aligned16(index)) return UQ_ERR_INVALID_ARG;
+  return asym_impl(q8, nq, ldq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace, workspace_bytes, stream,
+                   index);
 }
 
 uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d, unsigned long long* bad_rows,

@@ -89,6 +89,8 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             const int8_t* q8 = nullptr, int64_t ldq8 = 0, const uint8_t* dbx = nullptr);
 // E2M1 index (uq_build_f4_index): rows padded to whole 240-row pair tiles
 size_t f4_index_bytes(int64_t n, int32_t d);
+size_t i8_index_bytes(int64_t n, int32_t d);
+cudaError_t launch_build_i8_index(const uint8_t* codes, int64_t n, int32_t d, uint8_t* index, cudaStream_t st);
 cudaError_t launch_build_f4_index(const uint8_t* codes, int64_t n, int32_t d, uint8_t* index, cudaStream_t st);
 // int8 query quantisation (R15): per row scale 127 / max|u| (fp32), round half even
 cudaError_t launch_quantize_i8(const void* u, uq_dtype dt, int64_t n, int32_t d, int64_t ld, int8_t* out,

@@ -230,7 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
   uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps per set
   uint64_t* loaded = tempty + 2;           // [stages] (each CTA): bulk-copy transaction barriers (dbx mode)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(loaded + p.stages);
-  const bool xmode = OP == kOpF4 && p.dbx != nullptr;
+  const bool xmode = p.dbx != nullptr;
 
   // seed fallback pass with nothing to redo: every thread of both CTAs leaves
   if (p.any_fail != nullptr && *p.any_fail == 0) return;
@@ -383,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
             if (++stage == S) { stage = 0; sphase ^= 1u; }
           }
       } else if (leader && warp == kMmaWarp) {
-        constexpr uint32_t idesc = idesc_mxf4(2 * BM, BN);
+        constexpr uint32_t idesc = OP == kOpF4 ? idesc_mxf4(2 * BM, BN) : idesc_i8(2 * BM, BN);
         const uint32_t sf_tmem = tmem_base + G::SF_COL;
         const uint64_t a_desc0 = smem_desc(smem_u32(sA), A_LBO, SBO);
         const uint64_t b_desc0 = smem_desc(smem_u32(sB), B_LBO, SBO);
@@ -403,7 +403,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                   for (int kk = 0; kk < G::MPB; ++kk) {
                     const uint64_t ad = a_desc0 + (uint64_t)(((uint32_t)(kb * G::CPB + kk * 2) * A_LBO) >> 4);
                     const uint64_t bd = b_stage + (uint64_t)(((uint32_t)(bb * G::CPB + kk * 2) * B_LBO) >> 4);
-                    mma2_f4(d_tmem, ad, bd, idesc, sf_tmem, sf_tmem, (kb | kk) != 0 ? 1u : 0u);
+                    if (OP == kOpF4) mma2_f4(d_tmem, ad, bd, idesc, sf_tmem, sf_tmem, (kb | kk) != 0 ? 1u : 0u);
+                    else mma2_i8(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                   }
                 }
               }
@@ -917,7 +918,52 @@ __global__ void build_f4_index_kernel(const uint8_t* __restrict__ codes, int64_t
   }
 }
 
+// int8 index (single-operand search / the int8 engine): each 128-row half tile
+// as the int8 pair kernel's stage image -- [NB][8 chunks][16 row groups][8
+// rows][16 B], chunk 2w + h of block kb = bytes 16h.. of expand_word(word 4kb+w)
+// -- rows padded with zeros to whole 256-row tiles.
+__global__ void build_i8_index_kernel(const uint8_t* __restrict__ codes, int64_t n, int64_t n_pad, int NB,
+                                      uint8_t* __restrict__ index) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pad * NB) return;
+  const int64_t r = t / NB;
+  const int kb = (int)(t % NB);
+  const int64_t pb = (int64_t)NB * 16;
+  uint4 pw = make_uint4(0, 0, 0, 0), nw = pw;
+  if (r < n) {
+    pw = *reinterpret_cast<const uint4*>(codes + r * 2 * pb + kb * 16);
+    nw = *reinterpret_cast<const uint4*>(codes + r * 2 * pb + pb + kb * 16);
+  }
+  const uint32_t pp[4] = {pw.x, pw.y, pw.z, pw.w}, nn[4] = {nw.x, nw.y, nw.z, nw.w};
+  constexpr int HT = 128;
+  const int64_t h = r / HT;
+  const int j = (int)(r % HT);
+  uint8_t* base = index + (size_t)h * NB * 8 * HT * 16 + (size_t)kb * 8 * HT * 16 + (j >> 3) * 128 + (j & 7) * 16;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t o[8];
+    ::uq::tc::expand_word(pp[w], nn[w], o);
+    *reinterpret_cast<uint4*>(base + (size_t)(2 * w) * HT * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(base + (size_t)(2 * w + 1) * HT * 16) = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
 }  // namespace tc2
+
+size_t i8_index_bytes(int64_t n, int32_t d) {
+  const int64_t n_pad = (n + 255) / 256 * 256;
+  return (size_t)n_pad * blocks128(d) * 128;
+}
+
+cudaError_t launch_build_i8_index(const uint8_t* codes, int64_t n, int32_t d, uint8_t* index, cudaStream_t st) {
+  const int NB = blocks128(d);
+  const int64_t n_pad = (n + 255) / 256 * 256;
+  const int64_t threads = n_pad * NB;
+  if (threads == 0) return cudaSuccess;
+  tc2::build_i8_index_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(codes, n, n_pad, NB, index);
+  note_launch();
+  return cudaGetLastError();
+}
 
 size_t f4_index_bytes(int64_t n, int32_t d) {
   const int64_t n_pad = (n + 239) / 240 * 240;
@@ -1099,7 +1145,6 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st, const int32_t* qfail, const int32_t* any_fail, const int8_t* q8,
                             int64_t ldq8, const uint8_t* dbx) {
-  if (dbx != nullptr && op != tc2::kOpF4) return cudaErrorInvalidValue;
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(q8 ? 127 * d : d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
@@ -1114,7 +1159,6 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
                                  int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
                                  int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8, int64_t ldq8,
                                  const uint8_t* dbx) {
-  if (dbx != nullptr && op != tc2::kOpF4) return cudaErrorInvalidValue;
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;

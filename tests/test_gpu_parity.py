@@ -539,3 +539,25 @@ def test_search_f4_index_seed_fallback(uq, orc, monkeypatch, opt, k):
     s, i = uq.search(torch.from_numpy(o_q).cuda(), dbc, d, k, f4_index=uq.build_f4_index(dbc, d))
     s_ref, i_ref = orc.knn(o_q, o_db, d, k)
     assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
+
+
+@pytest.mark.parametrize("d,x,n,nq,k,mode", [(384, 192, 5000, 130, 10, "normal"), (768, 384, 20001, 300, 100, "dup"),
+                                             (1024, 512, 131072, 260, 10, "normal"), (129, 40, 241, 3, 7, "ties")])
+def test_search_asym_i8_index_parity(uq, orc, d, x, n, nq, k, mode):
+    """Single-operand search fed by the int8 index (bulk-copy stages) equals the
+    oracle's masked-addition kNN."""
+    rng = np.random.default_rng(d + n + 1)
+    if mode == "dup":
+        base = rng.standard_normal((max(1, n // 7), d)).astype(np.float32)
+        u_db = base[rng.integers(0, base.shape[0], size=n)]
+    elif mode == "ties":
+        u_db = _tie_heavy(rng, n, d)
+    else:
+        u_db = rng.standard_normal((n, d)).astype(np.float32)
+    u_q = rng.standard_normal((nq, d)).astype(np.float32)
+    o_db = orc.pack(orc.encode(u_db, x))
+    q8 = orc.quantize_i8(u_q)
+    dbc = torch.from_numpy(o_db).cuda()
+    s, i = uq.search_asym(torch.from_numpy(q8).cuda(), dbc, d, k, id_base=2, i8_index=uq.build_i8_index(dbc, d))
+    s_ref, i_ref = orc.knn_asym(q8, o_db, d, k, id_base=2)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
