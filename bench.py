@@ -286,8 +286,15 @@ def main():
     # like the encode) and every scan stage is one bulk copy
     i8x = uq.build_i8_index(dbc, d) if (asym and not args.no_f4_index and d <= 1024) else None
     f4x = None
+    idx_ms = None
     if not args.no_f4_index and not asym and uq.search_resolve(nq, n_loc, d, k, algo) == uq.ALGO_TC_FP4:
+        f4x = uq.build_f4_index(dbc, d)            # warm-up build
+        ib0, ib1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ib0.record()
         f4x = uq.build_f4_index(dbc, d)
+        ib1.record()
+        torch.cuda.synchronize()
+        idx_ms = ib0.elapsed_time(ib1)
     ws_bytes = uq.search_asym_workspace(nq, n_loc, d, k) if asym else uq.search_workspace(nq, n_loc, d, k, algo)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     q8 = torch.empty((nq, d), dtype=torch.int8, device=dev)
@@ -504,6 +511,7 @@ def main():
         "index": {"codes_bytes": n_loc * uq.code_bytes(d),
                   "f4_index_bytes": int(f4x.numel()) if f4x is not None else 0,
                   "i8_index_bytes": int(i8x.numel()) if i8x is not None else 0,
+                  "f4_index_build_ms": idx_ms,
                   "note": "E2M1 operand image of the codes (4 bits per dim), built once with the index"
                           if f4x is not None else "2-bit codes only"},
         "encode": {"rows_per_s": n_loc / (enc_ms * 1e-3), "GB_per_s": enc_bytes / (enc_ms * 1e-3) / 1e9,
