@@ -40,7 +40,7 @@ def _data(rng, n, d, mode):
     return rng.standard_normal((n, d)).astype(np.float32)
 
 
-@pytest.mark.parametrize("seed", range(160))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("UQ_FUZZ_N", "160"))))
 def test_fuzz_engines(uq, orc, seed):
     rng, d, x, n, nq, k, mode = _draw(seed)
     u_db = _data(rng, n, d, mode)
