@@ -75,3 +75,31 @@ def test_fuzz_engines(uq, orc, seed):
         s_ref, i_ref = orc.knn_asym(q8, o_db, d, k, id_base=11)
         assert np.array_equal(s.cpu().numpy(), s_ref), (seed, "asym", d, x, n, nq, k, mode)
         assert np.array_equal(i.cpu().numpy(), i_ref), (seed, "asym", d, x, n, nq, k, mode)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_seeded(uq, orc, seed):
+    """Random shapes large enough for threshold seeding (n >= 2^16): optimistic
+    histogram seeds, their verification and fallback, every engine."""
+    rng = np.random.default_rng(5000 + seed)
+    d = int(rng.choice([64, 128, 256, 384, 768]))
+    x = int(rng.integers(1, d + 1))
+    n = int(rng.choice([65536, 70001, 131072, 200003]))
+    nq = int(rng.choice([9, 130, 257, 300]))
+    k = int(rng.choice([1, 10, 100, 300]))
+    mode = str(rng.choice(["normal", "dup", "ties"]))
+    u_db, u_q = _data(rng, n, d, mode), _data(rng, nq, d, mode)
+    o_db, o_q = orc.pack(orc.encode(u_db, x)), orc.pack(orc.encode(u_q, x))
+    s_ref, i_ref = orc.knn(o_q, o_db, d, k)
+    qg, dbg = torch.from_numpy(o_q).cuda(), torch.from_numpy(o_db).cuda()
+    runs = [dict(algo=a) for a in (uq.ALGO_POPC, uq.ALGO_TCGEN05, uq.ALGO_TC_FP4, uq.ALGO_AUTO)]
+    runs.append(dict(f4_index=uq.build_f4_index(dbg, d)))
+    for kw in runs:
+        try:
+            uq.search_workspace(nq, n, d, k, kw.get("algo", uq.ALGO_TC_FP4))
+        except uq.UQError:
+            continue
+        s, i = uq.search(qg, dbg, d, k, **kw)
+        tag = (seed, tuple(kw), d, x, n, nq, k, mode)
+        assert np.array_equal(s.cpu().numpy(), s_ref), tag
+        assert np.array_equal(i.cpu().numpy(), i_ref), tag
