@@ -95,7 +95,11 @@ uq_status uq_scores(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, i
 
 /*
  * uq_search_workspace -- bytes of device workspace uq_search needs for this
- * shape on the CURRENT device (*bytes is a host pointer).
+ * shape on the CURRENT device (*bytes is a host pointer).  Sizing helper of
+ * uq_search (P:61 / P:480); the workspace holds the per-CTA top-k stream
+ * buffers, the per-chunk candidate lists of the merge and the threshold
+ * seed, never results.  Errors as uq_search's
+ * synchronous checks; UQ_ERR_UNSUPPORTED if no engine runs the shape.
  */
 uq_status uq_search_workspace(int64_t nq, int64_t n, int32_t d, int32_t k, size_t* bytes);
 uq_status uq_search_workspace_ex(int64_t nq, int64_t n, int32_t d, int32_t k, uq_algo algo,
@@ -137,16 +141,20 @@ uq_status uq_search_ex(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes
  * 2-bit -> E2M1 expansion by the producer warps; results are identical.
  *   uq_f4_index_bytes(n, d)                   size of the index (host call)
  *   uq_build_f4_index(dbcodes, n, d, index)   fills it (device buffers, 16-B aligned)
- *   uq_search_f4x(..., dbcodes, index, ...)   uq_search_ex(UQ_ALGO_TC_FP4) reading the
+ *   uq_search_f4x(..., dbcodes, index, index_bytes, ...)
+ *                                             uq_search_ex(UQ_ALGO_TC_FP4) reading the
  *                                             index (dbcodes still serves the
  *                                             workspace plan; d <= 1536)
- * Errors as uq_search_ex; UQ_ERR_UNSUPPORTED for d > 1536.
+ * index_bytes must equal uq_f4_index_bytes(n, d): an index built for another
+ * row count is rejected synchronously (UQ_ERR_INVALID_ARG) instead of being
+ * read out of bounds.  Other errors as uq_search_ex; UQ_ERR_UNSUPPORTED for
+ * d > 1536.
  */
 size_t uq_f4_index_bytes(int64_t n, int32_t d);
 uq_status uq_build_f4_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_t* index,
                             uq_stream_t stream);
 uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, const uint8_t* index,
-                        int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
+                        size_t index_bytes, int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
                         int64_t* out_ids, void* workspace, size_t workspace_bytes, uq_stream_t stream);
 
 /*
@@ -154,13 +162,15 @@ uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcode
  * bits per dim, 128-row half tiles as its stage image, rows padded to 256),
  * used by single-operand search.  d <= 1024.
  *   uq_i8_index_bytes(n, d), uq_build_i8_index(dbcodes, n, d, index)
- *   uq_search_asym_x(...)   uq_search_asym reading the index
+ *   uq_search_asym_x(..., index, index_bytes, ...)   uq_search_asym reading the
+ *                           index; index_bytes must equal uq_i8_index_bytes(n, d)
+ *                           (else UQ_ERR_INVALID_ARG)
  */
 size_t uq_i8_index_bytes(int64_t n, int32_t d);
 uq_status uq_build_i8_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_t* index,
                             uq_stream_t stream);
 uq_status uq_search_asym_x(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes,
-                           const uint8_t* index, int64_t n, int32_t d, int32_t k, int64_t id_base,
+                           const uint8_t* index, size_t index_bytes, int64_t n, int32_t d, int32_t k, int64_t id_base,
                            int32_t* out_scores, int64_t* out_ids, void* workspace,
                            size_t workspace_bytes, uq_stream_t stream);
 
@@ -190,9 +200,18 @@ uq_status uq_merge_topk_ptrs(const int32_t* const* score_ptrs, const int64_t* co
                              uq_stream_t stream);
 
 /*
- * uq_check_codes -- count rows that are not valid packed ternary codes: some
- * position set in both planes (pos AND neg != 0), or a pad bit (i >= d) set.
- * *bad_rows is a DEVICE uint64 scalar that the call overwrites.
+ * uq_check_codes -- count rows that are not valid packed ternary codes.  A
+ * code is an EVP vertex component-wise in {-1, 0, 1}, stored as the
+ * two bit planes v+ / v- of P:357 and P:379 ("positive and negative elements"
+ * of Table 3), so no position can be set in both planes; bits past
+ * d are the plane padding (reading R6 of DESIGN.md) and must be 0,
+ * which keeps b2sp padding-independent.  A row is counted if some
+ * position is set in both planes (pos AND neg != 0) or a pad bit (i >= d) is
+ * set.  *bad_rows is a DEVICE uint64 scalar that the call overwrites.  The
+ * search kernels assume valid codes (their 2-popcount identity needs
+ * pos AND neg = 0); this call is the on-demand check of that precondition.
+ * Errors: UQ_ERR_INVALID_ARG for n < 0, d < 1, a null bad_rows, or null /
+ * misaligned codes with n > 0; UQ_ERR_UNSUPPORTED for d > UQ_MAX_D.
  */
 uq_status uq_check_codes(const uint8_t* codes, int64_t n, int32_t d,
                          unsigned long long* bad_rows, uq_stream_t stream);

@@ -22,7 +22,9 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libuq.so")
+# tools/ may load the profile build (timing ablations compiled in) by setting
+# UQ_PROFILE_LIB=1 before import; everything else loads the product library.
+_LIB_PATH = os.path.join(_HERE, "libuq_prof.so" if os.environ.get("UQ_PROFILE_LIB") == "1" else "libuq.so")
 
 ALGO_AUTO, ALGO_POPC, ALGO_TCGEN05, ALGO_TC_FP4 = 0, 1, 2, 3
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -57,10 +59,10 @@ def _load():
     L.uq_merge_topk_ptrs.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp]
     L.uq_f4_index_bytes.argtypes, L.uq_f4_index_bytes.restype = [i64, i32], sz
     L.uq_build_f4_index.argtypes = [vp, i64, i32, vp, vp]
-    L.uq_search_f4x.argtypes = [vp, i64, vp, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
+    L.uq_search_f4x.argtypes = [vp, i64, vp, vp, sz, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_i8_index_bytes.argtypes, L.uq_i8_index_bytes.restype = [i64, i32], sz
     L.uq_build_i8_index.argtypes = [vp, i64, i32, vp, vp]
-    L.uq_search_asym_x.argtypes = [vp, i64, i64, vp, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
+    L.uq_search_asym_x.argtypes = [vp, i64, i64, vp, vp, sz, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_asym_workspace.argtypes = [i64, i64, i32, i32, ctypes.POINTER(sz)]
     L.uq_search_asym.argtypes = [vp, i64, i64, vp, i64, i32, i32, i64, vp, vp, vp, sz, vp]
     L.uq_search_resolve.argtypes = [i64, i64, i32, i32, i32, ctypes.POINTER(i32)]
@@ -128,6 +130,20 @@ def _stream(stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _empty(stream, *shape_args, **kw) -> torch.Tensor:
+    """torch.empty allocated ON `stream` (the stream the kernels run on): the
+    caching allocator then never hands the block to another stream's
+    allocation while this call's kernels may still be using it."""
+    if stream is None:
+        return torch.empty(*shape_args, **kw)
+    with torch.cuda.stream(stream):
+        return torch.empty(*shape_args, **kw)
+
+
+def _index_bytes(t: torch.Tensor) -> int:
+    return t.numel() * t.element_size()
+
+
 def _ptr(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() > 0 else 0)
 
@@ -152,7 +168,7 @@ def encode(u: torch.Tensor, x: int, out: Optional[torch.Tensor] = None, stream=N
         raise TypeError(f"unsupported dtype {u.dtype}")
     n, d = u.shape
     if out is None:
-        out = torch.empty((n, code_bytes(d)), dtype=torch.uint8, device=u.device)
+        out = _empty(stream, (n, code_bytes(d)), dtype=torch.uint8, device=u.device)
     _check("uq_encode", _L.uq_encode(_ptr(u), _DT[u.dtype], n, d, u.stride(0), x, _ptr(out),
                                      _stream(stream)))
     return out
@@ -162,7 +178,7 @@ def scores(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, stream=None) -> 
     """Dense Delta matrix [nq][n] int32 (uq_scores; test/debug)."""
     _dev(qcodes, "qcodes"); _dev(dbcodes, "dbcodes")
     nq, n = qcodes.shape[0], dbcodes.shape[0]
-    out = torch.empty((nq, n), dtype=torch.int32, device=qcodes.device)
+    out = _empty(stream, (nq, n), dtype=torch.int32, device=qcodes.device)
     _check("uq_scores", _L.uq_scores(_ptr(qcodes), nq, _ptr(dbcodes), n, d, _ptr(out),
                                      _stream(stream)))
     return out
@@ -185,7 +201,7 @@ def build_f4_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
     """E2M1 index of the database codes for the pair engine (uq_build_f4_index)."""
     _dev(dbcodes, "dbcodes")
     n = dbcodes.shape[0]
-    out = torch.empty(max(int(_L.uq_f4_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
+    out = _empty(stream, max(int(_L.uq_f4_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
     _check("uq_build_f4_index", _L.uq_build_f4_index(_ptr(dbcodes), n, d, _ptr(out), _stream(stream)))
     return out
 
@@ -194,7 +210,7 @@ def build_i8_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
     """int8 index of the database codes for single-operand search (uq_build_i8_index)."""
     _dev(dbcodes, "dbcodes")
     n = dbcodes.shape[0]
-    out = torch.empty(max(int(_L.uq_i8_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
+    out = _empty(stream, max(int(_L.uq_i8_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
     _check("uq_build_i8_index", _L.uq_build_i8_index(_ptr(dbcodes), n, d, _ptr(out), _stream(stream)))
     return out
 
@@ -210,14 +226,14 @@ def search(qcodes: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base:
     nq, n = qcodes.shape[0], dbcodes.shape[0]
     dev = qcodes.device
     if out is None:
-        out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
-               torch.empty((nq, k), dtype=torch.int64, device=dev))
+        out = (_empty(stream, (nq, k), dtype=torch.int32, device=dev),
+               _empty(stream, (nq, k), dtype=torch.int64, device=dev))
     need = search_workspace(nq, n, d, k, ALGO_TC_FP4 if f4_index is not None else algo)
     if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+        workspace = _empty(stream, max(need, 1), dtype=torch.uint8, device=dev)
     if f4_index is not None:
         _dev(f4_index, "f4_index")
-        _check("uq_search_f4x", _L.uq_search_f4x(_ptr(qcodes), nq, _ptr(dbcodes), _ptr(f4_index), n, d, k, id_base,
+        _check("uq_search_f4x", _L.uq_search_f4x(_ptr(qcodes), nq, _ptr(dbcodes), _ptr(f4_index), _index_bytes(f4_index), n, d, k, id_base,
                                                  _ptr(out[0]), _ptr(out[1]), _ptr(workspace), workspace.numel(),
                                                  _stream(stream)))
         return out
@@ -235,7 +251,7 @@ def quantize_i8(u: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None
         raise ValueError("u must be 2-D f32/f16/bf16 with unit column stride")
     n, d = u.shape
     if out is None:
-        out = torch.empty((n, d), dtype=torch.int8, device=u.device)
+        out = _empty(stream, (n, d), dtype=torch.int8, device=u.device)
     _check("uq_quantize_i8", _L.uq_quantize_i8(_ptr(u), _DT[u.dtype], n, d, u.stride(0), _ptr(out),
                                                out.stride(0), _stream(stream)))
     return out
@@ -259,14 +275,14 @@ def search_asym(q8: torch.Tensor, dbcodes: torch.Tensor, d: int, k: int, id_base
     nq, n = q8.shape[0], dbcodes.shape[0]
     dev = q8.device
     if out is None:
-        out = (torch.empty((nq, k), dtype=torch.int32, device=dev),
-               torch.empty((nq, k), dtype=torch.int64, device=dev))
+        out = (_empty(stream, (nq, k), dtype=torch.int32, device=dev),
+               _empty(stream, (nq, k), dtype=torch.int64, device=dev))
     need = search_asym_workspace(nq, n, d, k)
     if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+        workspace = _empty(stream, max(need, 1), dtype=torch.uint8, device=dev)
     if i8_index is not None:
         _dev(i8_index, "i8_index")
-        _check("uq_search_asym_x", _L.uq_search_asym_x(_ptr(q8), nq, q8.stride(0), _ptr(dbcodes), _ptr(i8_index), n,
+        _check("uq_search_asym_x", _L.uq_search_asym_x(_ptr(q8), nq, q8.stride(0), _ptr(dbcodes), _ptr(i8_index), _index_bytes(i8_index), n,
                                                        d, k, id_base, _ptr(out[0]), _ptr(out[1]), _ptr(workspace),
                                                        workspace.numel(), _stream(stream)))
         return out
@@ -285,8 +301,8 @@ def merge_topk(scores_g: torch.Tensor, ids_g: torch.Tensor, k: int,
     if kin != k:
         raise ValueError("lists must hold k entries per query")
     if out is None:
-        out = (torch.empty((nq, k), dtype=torch.int32, device=scores_g.device),
-               torch.empty((nq, k), dtype=torch.int64, device=scores_g.device))
+        out = (_empty(stream, (nq, k), dtype=torch.int32, device=scores_g.device),
+               _empty(stream, (nq, k), dtype=torch.int64, device=scores_g.device))
     _check("uq_merge_topk", _L.uq_merge_topk(_ptr(scores_g), _ptr(ids_g), g, nq, k, _ptr(out[0]),
                                              _ptr(out[1]), _stream(stream)))
     return out
@@ -303,8 +319,8 @@ def merge_topk_ptrs(score_ptrs: torch.Tensor, id_ptrs: torch.Tensor, nq: int, k:
         raise ValueError("pointer arrays must be int64 device tensors of equal length")
     g = score_ptrs.numel()
     if out is None:
-        out = (torch.empty((nq, k), dtype=torch.int32, device=score_ptrs.device),
-               torch.empty((nq, k), dtype=torch.int64, device=score_ptrs.device))
+        out = (_empty(stream, (nq, k), dtype=torch.int32, device=score_ptrs.device),
+               _empty(stream, (nq, k), dtype=torch.int64, device=score_ptrs.device))
     _check("uq_merge_topk_ptrs", _L.uq_merge_topk_ptrs(_ptr(score_ptrs), _ptr(id_ptrs), g, nq, k, _ptr(out[0]),
                                                        _ptr(out[1]), _stream(stream)))
     return out
@@ -323,8 +339,8 @@ def rerank(q: torch.Tensor, db: torch.Tensor, cand: torch.Tensor, k: int,
     nq, d = q.shape
     n_cand = cand.shape[1]
     if out is None:
-        out = (torch.empty((nq, k), dtype=torch.float32, device=q.device),
-               torch.empty((nq, k), dtype=torch.int64, device=q.device))
+        out = (_empty(stream, (nq, k), dtype=torch.float32, device=q.device),
+               _empty(stream, (nq, k), dtype=torch.int64, device=q.device))
     _check("uq_rerank", _L.uq_rerank(_ptr(q), _DT[q.dtype], nq, q.stride(0), _ptr(db), db.shape[0],
                                      db.stride(0), d, _ptr(cand), n_cand, k, _ptr(out[0]), _ptr(out[1]),
                                      _stream(stream)))
@@ -334,7 +350,9 @@ def rerank(q: torch.Tensor, db: torch.Tensor, cand: torch.Tensor, k: int,
 def check_codes(codes: torch.Tensor, d: int, stream=None) -> int:
     """Number of invalid code rows (uq_check_codes); synchronises to read the count."""
     _dev(codes, "codes")
-    bad = torch.zeros(1, dtype=torch.int64, device=codes.device)
+    bad = _empty(stream, 1, dtype=torch.int64, device=codes.device)
     _check("uq_check_codes", _L.uq_check_codes(_ptr(codes), codes.shape[0], d, _ptr(bad),
                                                _stream(stream)))
+    if stream is not None:
+        stream.synchronize()
     return int(bad.item())

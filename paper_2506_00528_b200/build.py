@@ -12,6 +12,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libuq.so")
+# Profile build (tools/ only): -DUQ_PROFILE compiles in the tensor scans'
+# timing ablations and cycle accounting (UQ_TC_ABLATE); the product libuq.so
+# never has them.
+LIB_PROF = os.path.join(HERE, "libuq_prof.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -24,9 +28,9 @@ def _deps():
                   + [os.path.join(HERE, "..", "include", "uq.h")])
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+def _compile(src: str, verbose: bool, profile: bool = False) -> str:
+    obj = os.path.join(OBJ, os.path.basename(src) + (".prof.o" if profile else ".o"))
+    cmd = [NVCC, *ARCH, *FLAGS, *(["-DUQ_PROFILE"] if profile else []), "-c", src, "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -37,9 +41,9 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def _src_hash() -> str:
+def _src_hash(profile: bool = False) -> str:
     import hashlib
-    h = hashlib.sha256()
+    h = hashlib.sha256(b"profile" if profile else b"")
     for p in _deps():
         h.update(os.path.basename(p).encode())
         with open(p, "rb") as f:
@@ -48,29 +52,30 @@ def _src_hash() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
     """Compile if the library is missing or its recorded source hash differs
     (content-based: file mtimes do not survive the snapshot to the GPU box)."""
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    stamp = LIB + ".srchash"
-    digest = _src_hash()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp):
+    lib = LIB_PROF if profile else LIB
+    stamp = lib + ".srchash"
+    digest = _src_hash(profile)
+    if not force and os.path.exists(lib) and os.path.exists(stamp):
         with open(stamp) as f:
             if f.read().strip() == digest:
                 return LIB
     os.makedirs(OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda s: _compile(s, verbose, profile), srcs))
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     with open(stamp, "w") as f:
         f.write(digest + "\n")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

@@ -288,11 +288,14 @@ uq_status uq_timing_enable(int32_t on) {
   return UQ_OK;
 }
 
-// Debug (not in uq.h): CTA-pair scan cycle accounting under UQ_TC_ABLATE & 8.
+#ifdef UQ_PROFILE
+// Profile builds only (libuq_prof.so, not in uq.h): CTA-pair scan cycle
+// accounting under UQ_TC_ABLATE & 8.
 uq_status uq_debug_tc2_prof(unsigned long long* out48) {
   if (!out48) return UQ_ERR_INVALID_ARG;
   return from_cuda(tc2_prof_read(out48));
 }
+#endif
 
 uq_status uq_timing_collect_ex(double* scan_ms, int64_t* launches, double* delta_evals) {
   if (!scan_ms || !launches || !delta_evals) return UQ_ERR_INVALID_ARG;
@@ -463,10 +466,12 @@ uq_status uq_build_f4_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_
   return from_cuda(launch_build_f4_index(dbcodes, n, d, index, (cudaStream_t)stream));
 }
 
-uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, const uint8_t* index, int64_t n,
-                        int32_t d, int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
-                        void* workspace, size_t workspace_bytes, uq_stream_t stream) {
-  if (index == nullptr || !aligned16(index)) return UQ_ERR_INVALID_ARG;
+uq_status uq_search_f4x(const uint8_t* qcodes, int64_t nq, const uint8_t* dbcodes, const uint8_t* index,
+                        size_t index_bytes, int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
+                        int64_t* out_ids, void* workspace, size_t workspace_bytes, uq_stream_t stream) {
+  g_launches = 0;
+  if (n > 0 && d >= 1 && d <= UQ_MAX_D && index_bytes != f4_index_bytes(n, d)) return UQ_ERR_INVALID_ARG;
+  if (n > 0 && (index == nullptr || !aligned16(index))) return UQ_ERR_INVALID_ARG;
   return search_impl(qcodes, nq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace, workspace_bytes,
                      UQ_ALGO_TC_FP4, stream, index);
 }
@@ -651,9 +656,11 @@ uq_status uq_build_i8_index(const uint8_t* dbcodes, int64_t n, int32_t d, uint8_
 }
 
 uq_status uq_search_asym_x(const int8_t* q8, int64_t nq, int64_t ldq, const uint8_t* dbcodes, const uint8_t* index,
-                           int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores, int64_t* out_ids,
-                           void* workspace, size_t workspace_bytes, uq_stream_t stream) {
-  if (index == nullptr || !aligned16(index)) return UQ_ERR_INVALID_ARG;
+                           size_t index_bytes, int64_t n, int32_t d, int32_t k, int64_t id_base, int32_t* out_scores,
+                           int64_t* out_ids, void* workspace, size_t workspace_bytes, uq_stream_t stream) {
+  g_launches = 0;
+  if (n > 0 && d >= 1 && d <= UQ_MAX_D && index_bytes != i8_index_bytes(n, d)) return UQ_ERR_INVALID_ARG;
+  if (n > 0 && (index == nullptr || !aligned16(index))) return UQ_ERR_INVALID_ARG;
   return asym_impl(q8, nq, ldq, dbcodes, n, d, k, id_base, out_scores, out_ids, workspace, workspace_bytes, stream,
                    index);
 }

@@ -7,7 +7,21 @@
 
 #include "../../include/uq.h"
 
+// Timing ablations and cycle accounting of the tensor scans (tools/ only).
+// The product library is built WITHOUT UQ_PROFILE: UQ_DBG(p) is the constant 0,
+// every ablation / profiling branch is compiled out, and no environment
+// variable can change a result.  `python paper_2506_00528_b200/build.py
+// --profile` builds libuq_prof.so with them for tools/tc2_prof.py.
+#ifdef UQ_PROFILE
+#define UQ_DBG(p) ((p).dbg)
+#else
+#define UQ_DBG(p) 0
+#endif
+
 namespace uq {
+
+// env UQ_TC_ABLATE in profile builds, 0 otherwise
+int tc_ablate_flags();
 
 void note_launch(int n = 1);
 

@@ -31,7 +31,8 @@ struct MergeParams {
   int64_t nq;
   int32_t kin;      // entries per list per query
   int32_t k;        // output k
-  int64_t id_base;  // added to rows of source (a)
+  int64_t id_base;  // added to every output row (source (a): the shard's first row; (b): 0, or the
+                    // shard's first row at level 2 of a two-level merge, whose level 1 keeps local rows)
   int32_t* out_s;
   int64_t* out_id;
   int32_t stage_cap;  // candidates staged in shared memory if C <= stage_cap
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
     for (int j = 0; j < nsel; ++j) rank += (s_sel[j] > key) ? 1 : 0;
     const size_t o = (size_t)q * p.k + rank;
     p.out_s[o] = key_score(key);
-    p.out_id[o] = (FROM_SI ? 0 : p.id_base) + key_row(key);
+    p.out_id[o] = p.id_base + key_row(key);
   }
   for (int i = nsel + threadIdx.x; i < p.k; i += kMergeThreads) {
     const size_t o = (size_t)q * p.k + i;
@@ -291,9 +292,10 @@ cudaError_t launch_merge_keys(const uint64_t* keys, int64_t lists, int64_t nq, i
       p1.out_s = ss;
       p1.out_id = si;
       p1.lpg = lpg;
+      p1.id_base = 0;   // level 1 keeps local rows (< 2^32 - 1): global_key() repacks them at level 2
       cudaError_t e = launch_merge_common(p1, false, st, (unsigned)g);
       if (e != cudaSuccess) return e;
-      MergeParams p2{nullptr, ss, si, g, nq, k, k, 0, out_s, out_id, 0, nullptr, only, any, nullptr, nullptr, 0};
+      MergeParams p2{nullptr, ss, si, g, nq, k, k, id_base, out_s, out_id, 0, nullptr, only, any, nullptr, nullptr, 0};
       return launch_merge_common(p2, true, st);
     }
   }

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1) scan_tc_kernel(Params p)
       uint4 dp[NB], dn[NB];
       auto load_block = [&](int tile, int kb, uint4& a, uint4& b) {
         const int64_t lr = (int64_t)tile * BN + r;
-        if (tile < ntiles && lr < rows && !(p.dbg & 4)) {
+        if (tile < ntiles && lr < rows && !(UQ_DBG(p) & 4)) {
           const uint8_t* src = p.db + (row0 + lr) * p.row_stride * cb;
           a = __ldg(reinterpret_cast<const uint4*>(src) + kb);
           b = __ldg(reinterpret_cast<const uint4*>(src + pb) + kb);
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1) scan_tc_kernel(Params p)
         for (int kb = 0; kb < NB; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), sphase ^ 1u);
           uint8_t* dst = sB + (size_t)stage * kStageBytes + (r >> 3) * SBO + (r & 7) * 16;
-          if (!(p.dbg & 1)) expand_block_store(dp[kb], dn[kb], dst, B_LBO);
+          if (!(UQ_DBG(p) & 1)) expand_block_store(dp[kb], dn[kb], dst, B_LBO);
           fence_proxy_async();
           mbar_arrive(smem_u32(&full[stage]));
           if (++stage == S) { stage = 0; sphase ^= 1u; }
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1) scan_tc_kernel(Params p)
         const int64_t lr0 = (int64_t)tile * BN;
         const int ncols = (rows - lr0 < BN) ? (int)(rows - lr0) : BN;
 #pragma unroll 1
-        for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : BN); c0 += 32) {
+        for (int c0 = 0; c0 < ((UQ_DBG(p) & 2) ? 0 : BN); c0 += 32) {
           uint32_t v[32];
           tmem_ld32(tbase + (uint32_t)c0, v);
           if (ncols - c0 < 32) {  // ragged tail (warp-uniform): mask columns past the chunk
@@ -414,10 +414,7 @@ cudaError_t launch_scan_tc(const uint8_t* q, int64_t nq, const uint8_t* db, int6
                            const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
                            cudaStream_t st) {
   const int NB = blocks128(d);
-  static const int dbg = [] {
-    const char* e = getenv("UQ_TC_ABLATE");
-    return e ? atoi(e) : 0;
-  }();
+  const int dbg = tc_ablate_flags();
   tc::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                (int32_t)pl.n_chunks, pl.n_items, pl.cap, pl.stages, bufs, part, thr0, thr0_stride,
                row_stride, dbg};

@@ -143,7 +143,7 @@ struct Params {
 // 15 appended candidates, 16 in-loop stream cuts, 17 streams cut at the end.
 __device__ unsigned long long g_prof[48];   // [0, 24): top-k mode, [24, 48): histogram mode
 __device__ __forceinline__ long long clk() { return clock64(); }
-#define PROF_ON ((p.dbg & 8) != 0)
+#define PROF_ON ((UQ_DBG(p) & 8) != 0)
 #define PROF_ADD(i, v) do { if (PROF_ON && lane == 0) atomicAdd(&g_prof[(i) + (MODE == kModeHist ? 24 : 0)], (unsigned long long)(v)); } while (0)
 
 struct Item {
@@ -353,10 +353,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
       // warp 3 of the leader issues the MMAs.
       const uint32_t full_dst = mapa(smem_u32(&full[0]), 0);
       constexpr uint32_t kHalfTileBytes = (uint32_t)NB * G::CPB * BH * 16;
-      auto half_tile = [&](int tile) -> int64_t {   // global 120-row half-tile index of (tile, this CTA)
-        const int64_t sr = (int64_t)tile * BN + (int64_t)cr * BH;
+      auto half_tile = [&](int tile) -> int64_t {   // global half-tile index of (tile, this CTA)
+        // the same scan-row -> database-row map as the producers' sample_row:
+        // histogram mode takes whole BN-row blocks, one in every row_stride;
+        // top-k mode rows (row0 + sr) * row_stride (row_stride is 1 whenever an
+        // index is read in top-k mode).  row0 and tile offsets are multiples of BH.
+        const int64_t sr = row0 + (int64_t)tile * BN + (int64_t)cr * BH;
         const int64_t row = MODE == kModeHist ? (sr / BN) * (BN * p.row_stride) + sr % BN : sr * p.row_stride;
-        return (row0 + row) / BH;   // row0 and BN-row blocks are multiples of BH
+        return row / BH;
       };
       if (warp == 0 && lane == 0) {
         for (int tile = 0; tile < ntiles; ++tile) {
@@ -440,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
       // per tile: the per-block loads then cost no address arithmetic
       auto row_src = [&](int tile) -> const uint8_t* {
         const int64_t lr = (int64_t)tile * BN + (int64_t)cr * BH + r;
-        if (tile < ntiles && lr < rows && r < BH && !(p.dbg & 4)) return p.db + sample_row(row0 + lr) * cb;
+        if (tile < ntiles && lr < rows && r < BH && !(UQ_DBG(p) & 4)) return p.db + sample_row(row0 + lr) * cb;
         return nullptr;
       };
       auto load_block = [&](const uint8_t* src, int kb, uint4& a, uint4& b) {
@@ -489,16 +493,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           for (int bb = 0; bb < kBlkPerStage; ++bb) {
             const int kb = ks * kBlkPerStage + bb;
             if (kb < NB) {
-              if (!(p.dbg & 1) && r < BH && !(issuer && (p.dbg & 512))) {   // (512: ablation, issuer skips its rows)
+              if (!(UQ_DBG(p) & 1) && r < BH && !(issuer && (UQ_DBG(p) & 512))) {   // (512: ablation, issuer skips its rows)
                 if (OP == kOpF4)
-                  expand_block_store_f4(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(p.dbg & 32));
+                  expand_block_store_f4(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(UQ_DBG(p) & 32));
                 else
-                  expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(p.dbg & 32));
+                  expand_block_store(dp[kb], dn[kb], sdst + (size_t)(bb * G::CPB) * B_LBO, B_LBO, !(UQ_DBG(p) & 32));
               }
               load_block(nsrc, kb, dp[kb], dn[kb]);
             }
           }
-          if (!(p.dbg & 16)) fence_proxy_async();
+          if (!(UQ_DBG(p) & 16)) fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(full_dst + (uint32_t)stage * 8u);
           if (issuer) {
@@ -609,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           const int64_t lr0 = (int64_t)tile * BN + h * CW;
           const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
 #pragma unroll 1
-          for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
+          for (int c0 = 0; c0 < ((UQ_DBG(p) & 2) ? 0 : CW); c0 += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + (uint32_t)c0, v);
             if (OP == kOpF4 && !raw) {
@@ -669,11 +673,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           }
         }
         named_bar_sync(1 + quarter, 32 * kEpiSets);
-        const long long tf0 = (p.dbg & 8) ? clk() : 0;
-        if (h == 0) hist_flush<kHistBins>(s_hist, col, (qme < p.nq && !(p.dbg & 64)) ? p.ghist + (size_t)qme * kHistBinsMax : nullptr);
+        const long long tf0 = (UQ_DBG(p) & 8) ? clk() : 0;
+        if (h == 0) hist_flush<kHistBins>(s_hist, col, (qme < p.nq && !(UQ_DBG(p) & 64)) ? p.ghist + (size_t)qme * kHistBinsMax : nullptr);
         named_bar_sync(1 + quarter, 32 * kEpiSets);
-        if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[18], (unsigned long long)(clk() - tf0));
-        if ((p.dbg & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[19], 1ull);
+        if ((UQ_DBG(p) & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[18], (unsigned long long)(clk() - tf0));
+        if ((UQ_DBG(p) & 8) && lane == 0 && h == 0) atomicAdd(&g_prof[19], 1ull);
       } else {
         const int sidx = h * BM + quarter * 32; // first stream of this warp
         uint32_t* const wbufs = p.bufs + ((size_t)blockIdx.x * kEpiSets * BM + sidx) * p.cap;
@@ -702,7 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           const uint32_t pad = (OP == kOpF4 && !raw) ? 0u : 0x80000000u;
           const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
 #pragma unroll 1
-          for (int c0 = 0; c0 < ((p.dbg & 2) ? 0 : CW); c0 += 32) {
+          for (int c0 = 0; c0 < ((UQ_DBG(p) & 2) ? 0 : CW); c0 += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + (uint32_t)c0, v);
             if (OP == kOpF4 && !raw) {
@@ -1124,13 +1128,18 @@ static cudaError_t launch_tc2_mode(const tc2::Params& p, const TcPlan& pl, int N
                           : launch_tc2_op<MODE, tc2::kOpI8>(p, pl, NB, st);
 }
 
-static int tc2_dbg() {
+int tc_ablate_flags() {
+#ifdef UQ_PROFILE
   static const int dbg = [] {
     const char* e = getenv("UQ_TC_ABLATE");
     return e ? atoi(e) : 0;
   }();
   return dbg;
+#else
+  return 0;
+#endif
 }
+static int tc2_dbg() { return tc_ablate_flags(); }
 
 // profiling counters (dbg & 8): copy out and reset
 cudaError_t tc2_prof_read(unsigned long long* out48) {
@@ -1146,6 +1155,9 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             cudaStream_t st, const int32_t* qfail, const int32_t* any_fail, const int8_t* q8,
                             int64_t ldq8, const uint8_t* dbx) {
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
+  // an index is read by whole contiguous half tiles: top-k scans of an
+  // index are over every row (strided top-k scans only seed the other engines)
+  if (dbx != nullptr && row_stride != 1) return cudaErrorInvalidValue;
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(q8 ? 127 * d : d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
                 thr0_stride, row_stride, nullptr, 0.f, nullptr, 0.f, qfail, any_fail, q8, ldq8, dbx, tc2_dbg()};

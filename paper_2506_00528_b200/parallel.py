@@ -29,6 +29,20 @@ def shard_bounds(n: int, world: int, rank: int) -> Tuple[int, int]:
     return lo, hi
 
 
+def result_digest(results) -> str:
+    """SHA-256 over the bytes of the final [Q][k] (scores, ids) of every
+    result in `results` (an iterable of (scores, ids) tensor pairs, in order).
+    The search result is unique (total order (Delta desc, id asc)), so the
+    digest must be identical for every GPU count G, engine and launch shape:
+    bench.py prints it so the scaling runs can be checked for byte equality."""
+    import hashlib
+    h = hashlib.sha256()
+    for s, i in results:
+        h.update(s.detach().to("cpu", torch.int32).contiguous().numpy().tobytes())
+        h.update(i.detach().to("cpu", torch.int64).contiguous().numpy().tobytes())
+    return h.hexdigest()
+
+
 def allgather_lists(scores: torch.Tensor, ids: torch.Tensor, group=None):
     """[Q][k] per rank -> [G][Q][k] on every rank (one collective per tensor)."""
     world = dist.get_world_size(group)
@@ -79,9 +93,11 @@ class PeerExchange:
 
 def sharded_search(qcodes: torch.Tensor, db_shard: torch.Tensor, d: int, k: int, id_base: int,
                    group=None, search_fn: Optional[Callable] = None,
-                   merge_fn: Optional[Callable] = None, **search_kw):
+                   merge_fn: Optional[Callable] = None, merge_out=None, exchange=None, **search_kw):
     """Local search on this rank's shard + allgather + merge.  Returns the global
-    (scores [Q][k], ids [Q][k]) on every rank."""
+    (scores [Q][k], ids [Q][k]) on every rank.  `merge_out` (optional) receives
+    the merged result; `exchange` (optional, e.g. PeerExchange.merge) replaces
+    the allgather + merge with one peer-memory merge."""
     if search_fn is None or merge_fn is None:
         import paper_2506_00528_b200 as uq
         search_fn = search_fn or uq.search
@@ -89,5 +105,7 @@ def sharded_search(qcodes: torch.Tensor, db_shard: torch.Tensor, d: int, k: int,
     s, i = search_fn(qcodes, db_shard, d, k, id_base=id_base, **search_kw)
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return s, i
+    if exchange is not None:
+        return exchange(s, i)
     sg, ig = allgather_lists(s, i, group)
-    return merge_fn(sg, ig, k)
+    return merge_fn(sg, ig, k) if merge_out is None else merge_fn(sg, ig, k, out=merge_out)

@@ -62,3 +62,25 @@ def test_invalid_arguments_rejected_synchronously(L):
     assert L.uq_merge_topk(fake, fake, -1, 4, 5, fake, fake, None) == 1
     L.uq_check_codes.argtypes = [vp, i64, i32, vp, vp]
     assert L.uq_check_codes(fake, 10, 384, None, None) == 1
+
+
+def test_index_size_checked_synchronously(L):
+    """uq_search_f4x / uq_search_asym_x reject an index whose byte size does not
+    match (n, d): a stale index fails before any launch instead of being read
+    out of bounds."""
+    i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
+    fake = vp(0x1000)
+    L.uq_f4_index_bytes.argtypes, L.uq_f4_index_bytes.restype = [i64, i32], sz
+    L.uq_i8_index_bytes.argtypes, L.uq_i8_index_bytes.restype = [i64, i32], sz
+    L.uq_search_f4x.argtypes = [vp, i64, vp, vp, sz, i64, i32, i32, i64, vp, vp, vp, sz, vp]
+    L.uq_search_asym_x.argtypes = [vp, i64, i64, vp, vp, sz, i64, i32, i32, i64, vp, vp, vp, sz, vp]
+    n, d = 100000, 768
+    good = L.uq_f4_index_bytes(n, d)
+    assert good == (n + 239) // 240 * 240 * 6 * 64
+    stale = L.uq_f4_index_bytes(n - 1000, d)
+    assert L.uq_search_f4x(fake, 300, fake, fake, stale, n, d, 10, 0, fake, fake, fake, 1 << 30, None) == 1
+    assert L.uq_search_f4x(fake, 300, fake, fake, good + 64, n, d, 10, 0, fake, fake, fake, 1 << 30, None) == 1
+    assert L.uq_search_f4x(fake, 300, fake, None, good, n, d, 10, 0, fake, fake, fake, 1 << 30, None) == 1
+    gi = L.uq_i8_index_bytes(n, d)
+    assert gi == (n + 255) // 256 * 256 * 6 * 128
+    assert L.uq_search_asym_x(fake, 300, d, fake, fake, gi - 1, n, d, 10, 0, fake, fake, fake, 1 << 30, None) == 1

@@ -561,3 +561,57 @@ def test_search_asym_i8_index_parity(uq, orc, d, x, n, nq, k, mode):
     s, i = uq.search_asym(torch.from_numpy(q8).cuda(), dbc, d, k, id_base=2, i8_index=uq.build_i8_index(dbc, d))
     s_ref, i_ref = orc.knn_asym(q8, o_db, d, k, id_base=2)
     assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
+
+
+@pytest.mark.parametrize("engine", ["f4x", "asym_x"])
+@pytest.mark.parametrize("k", [2, 5, 8])
+def test_index_seed_samples_spread_rows(uq, orc, engine, k):
+    """Index-fed seeding scans (E2M1 / int8 index) must sample the same rows as
+    the producer path: whole row blocks spread over the WHOLE database, each
+    once (the bulk-copy path once sampled only the first rows, some
+    several times).  k <= 8 gives exact seeds (need = k, no verification), so a
+    row counted twice raises the bound above what the database supports and the
+    search returns fewer than k rows.  Each of the first 16 queries gets k - 1
+    planted copies (Delta = nnz, the maximum) at the start of sample block 1
+    (row 3840 = 240 rows x stride 16; with the wrong mapping two chunks' items
+    both read it); the remaining best rows are ordinary."""
+    rng = np.random.default_rng(100 + k)
+    d, x, n, nq = 128, 64, 1 << 20, 300
+    u_db = rng.standard_normal((n, d)).astype(np.float32)
+    u_q = rng.standard_normal((nq, d)).astype(np.float32)
+    for j in range(16):
+        for m in range(k - 1):
+            u_db[3840 + j * (k - 1) + m] = u_q[j] * (1.0 + 0.001 * m)   # same code as the query
+    for blk in (1, 2, 7):   # further planted copies at other block starts (2x-read rows under the old mapping)
+        for m in range(k - 1):
+            u_db[blk * 4096 + 7680 + m] = u_q[16] * (1.0 + 0.001 * m)
+    o_db = orc.pack(orc.encode(u_db, x))
+    dbc = torch.from_numpy(o_db).cuda()
+    if engine == "f4x":
+        o_q = orc.pack(orc.encode(u_q, x))
+        s, i = uq.search(torch.from_numpy(o_q).cuda(), dbc, d, k, f4_index=uq.build_f4_index(dbc, d))
+        s2, i2 = uq.search(torch.from_numpy(o_q).cuda(), dbc, d, k, algo=uq.ALGO_TC_FP4)
+        s_ref, i_ref = orc.knn(o_q, o_db, d, k)
+    else:
+        q8 = orc.quantize_i8(u_q)
+        s, i = uq.search_asym(torch.from_numpy(q8).cuda(), dbc, d, k, i8_index=uq.build_i8_index(dbc, d))
+        s2, i2 = uq.search_asym(torch.from_numpy(q8).cuda(), dbc, d, k)
+        s_ref, i_ref = orc.knn_asym(q8, o_db, d, k)
+    assert (i.cpu().numpy() >= 0).all(), "padding returned: the seed bound was above the k-th best row"
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)
+    assert torch.equal(s, s2) and torch.equal(i, i2)   # index-fed == producer-fed
+
+
+@pytest.mark.parametrize("algo,nq,k", [("popc", 1, 100), ("popc", 3, 10), ("auto", 2, 1000), ("f4", 300, 10)])
+def test_search_id_base_above_2_32(uq, orc, algo, nq, k):
+    """ids = id_base + row for id_base + n > 2^32 (the two-level
+    merge used for few queries once repacked id_base + row into 32 bits)."""
+    rng = np.random.default_rng(7 + nq)
+    d, x, n = 256, 128, 70001
+    base = (1 << 33) + 12345
+    o_db = orc.pack(orc.encode(rng.standard_normal((n, d)).astype(np.float32), x))
+    o_q = orc.pack(orc.encode(rng.standard_normal((nq, d)).astype(np.float32), x))
+    s, i = uq.search(torch.from_numpy(o_q).cuda(), torch.from_numpy(o_db).cuda(), d, k, id_base=base,
+                     algo=_algo(uq, algo))
+    s_ref, i_ref = orc.knn(o_q, o_db, d, k, id_base=base)
+    assert np.array_equal(s.cpu().numpy(), s_ref) and np.array_equal(i.cpu().numpy(), i_ref)

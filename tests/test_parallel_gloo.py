@@ -81,3 +81,54 @@ def test_shard_bounds():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[r][1] == b[r + 1][0] for r in range(w - 1))
             assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
+
+
+def _digest_worker(rank, world, port, ret):
+    """bench.py's strong-shard step on CPU stand-ins: shard_bounds -> local
+    search with id_base -> sharded_search (allgather + merge) -> result_digest."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import oracle as orc
+    from paper_2506_00528_b200.parallel import result_digest, shard_bounds, sharded_search
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    d, n, nq, k = 128, 5003, 17, 10
+    u = rng.standard_normal((n + nq, d))
+    u[100:140] = u[4000]                      # duplicates across shards: ties broken by id
+    res = []
+    for x in (32, 64, 96):                    # an x sweep, one digest over all of it
+        codes = orc.pack(orc.encode(u, x))
+        db, q = codes[:n], codes[n:]
+        lo, hi = shard_bounds(n, world, rank)
+        res.append(sharded_search(torch.from_numpy(q), torch.from_numpy(db[lo:hi]), d, k, id_base=lo,
+                                  search_fn=_cpu_search(orc), merge_fn=_cpu_merge))
+    ret[rank] = result_digest(res)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_strong_shard_digest_equal_across_world(world):
+    """The digest bench.py prints is the same for every GPU count: the merged
+    result is unique (byte-identical across G)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle as orc
+    from paper_2506_00528_b200.parallel import result_digest
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    mp.start_processes(_digest_worker, args=(world, _free_port(), ret), nprocs=world,
+                       start_method="spawn", join=True)
+    rng = np.random.default_rng(11)
+    d, n, nq, k = 128, 5003, 17, 10
+    u = rng.standard_normal((n + nq, d))
+    u[100:140] = u[4000]
+    ref = []
+    for x in (32, 64, 96):
+        codes = orc.pack(orc.encode(u, x))
+        s, i = orc.knn(codes[n:], codes[:n], d, k)
+        ref.append((torch.from_numpy(s), torch.from_numpy(i)))
+    want = result_digest(ref)
+    assert dict(ret) == {r: want for r in range(world)}

@@ -17,9 +17,10 @@ import datagen
 
 
 def cosine_topk_fp32(w, q_rows: torch.Tensor, k: int, id_base: int = 0, n: int | None = None,
-                     chunk: int = 1 << 16):
+                     chunk: int = 1 << 16, db_rows: torch.Tensor | None = None):
     """Exact cosine top-k of the float queries q_rows [Q][d] against database rows
-    [id_base, id_base + n) of workload w: (cos [Q][k] fp32, ids [Q][k] int64)."""
+    [id_base, id_base + n) of workload w: (cos [Q][k] fp32, ids [Q][k] int64).
+    `db_rows` (optional): those rows already resident ([n][d]), else regenerated."""
     n = w.n if n is None else n
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -30,7 +31,7 @@ def cosine_topk_fp32(w, q_rows: torch.Tensor, k: int, id_base: int = 0, n: int |
         best_i = torch.full((q.shape[0], k), -1, dtype=torch.int64, device=q.device)
         for s0 in range(0, n, chunk):
             c = min(chunk, n - s0)
-            u = datagen.rows(w, "db", id_base + s0, c, q.device).float()
+            u = (db_rows[s0:s0 + c] if db_rows is not None else datagen.rows(w, "db", id_base + s0, c, q.device)).float()
             u = u / u.norm(dim=1, keepdim=True)
             sc = q @ u.T                                   # [Q][c] fp32
             ids = torch.arange(id_base + s0, id_base + s0 + c, device=q.device).expand(q.shape[0], c)

@@ -1,5 +1,9 @@
 import os, sys, json, ctypes
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["UQ_PROFILE_LIB"] = "1"   # the profile build: ablations compiled in (libuq.so ignores UQ_TC_ABLATE)
+import importlib.util as _ilu  # noqa: E402
+_spec = _ilu.spec_from_file_location("_uqb", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2506_00528_b200", "build.py"))
+_m = _ilu.module_from_spec(_spec); _spec.loader.exec_module(_m); _m.build(profile=True)  # noqa: E702
 import torch, datagen, paper_2506_00528_b200 as uq
 w = datagen.CONFIGS['c2']
 db = uq.encode(datagen.db(w, 'cuda'), w.x); q = uq.encode(datagen.queries(w, 'cuda'), w.x)

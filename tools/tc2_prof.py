@@ -6,6 +6,10 @@ import json
 import os
 import sys
 
+os.environ["UQ_PROFILE_LIB"] = "1"   # the profile build: ablations compiled in (libuq.so ignores UQ_TC_ABLATE)
+import importlib.util as _ilu  # noqa: E402
+_spec = _ilu.spec_from_file_location("_uqb", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2506_00528_b200", "build.py"))
+_m = _ilu.module_from_spec(_spec); _spec.loader.exec_module(_m); _m.build(profile=True)  # noqa: E702
 os.environ["UQ_TC_ABLATE"] = str(int(os.environ.get("UQ_TC_ABLATE", "0")) | 8)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402

@@ -3,6 +3,10 @@ ablated modes; timing only).  Mode via env UQ_TC_ABLATE read at first launch,
 so each mode runs in its own process."""
 import os, sys, subprocess, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["UQ_PROFILE_LIB"] = "1"   # the profile build: ablations compiled in (libuq.so ignores UQ_TC_ABLATE)
+import importlib.util as _ilu  # noqa: E402
+_spec = _ilu.spec_from_file_location("_uqb", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2506_00528_b200", "build.py"))
+_m = _ilu.module_from_spec(_spec); _spec.loader.exec_module(_m); _m.build(profile=True)  # noqa: E702
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     import torch, paper_2506_00528_b200 as uq
     d, x, n, nq, k = 768, 384, int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
