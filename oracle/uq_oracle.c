@@ -155,22 +155,44 @@ static int cmp_cand(const void* a, const void* b) {
   return (x->id < y->id) ? -1 : (x->id > y->id) ? 1 : 0;
 }
 
+/* one query: Delta against every row (rows in parallel: each row's
+   arithmetic is untouched), then the plain sort, then the first k */
+static void knn_one(const uint8_t* q, const uint8_t* dc, int64_t n, int32_t d, int32_t k, int64_t id_base,
+                    int rows_parallel, int32_t* out_s, int64_t* out_id) {
+  const int64_t cb = orc_code_bytes(d);
+  orc_cand_t* c = (orc_cand_t*)malloc(sizeof(orc_cand_t) * (size_t)(n > 0 ? n : 1));
+#pragma omp parallel for schedule(static) if (rows_parallel)
+  for (int64_t r = 0; r < n; ++r) {
+    c[r].s = orc_b2sp(q, dc + r * cb, d);
+    c[r].id = id_base + r;
+  }
+  qsort(c, (size_t)n, sizeof(orc_cand_t), cmp_cand);
+  for (int32_t j = 0; j < k; ++j) {
+    out_s[j] = (j < n) ? c[j].s : INT32_MIN;
+    out_id[j] = (j < n) ? c[j].id : -1;
+  }
+  free(c);
+}
+
+/* threads of the OpenMP loops (1 without OpenMP) */
+static int orc_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
 void orc_knn(const uint8_t* qc, int64_t nq, const uint8_t* dc, int64_t n, int32_t d, int32_t k,
              int64_t id_base, int32_t* out_s, int64_t* out_id) {
   const int64_t cb = orc_code_bytes(d);
+  if (nq >= orc_threads()) {
+    /* many queries: one query per thread */
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t q = 0; q < nq; ++q) {
-    orc_cand_t* c = (orc_cand_t*)malloc(sizeof(orc_cand_t) * (size_t)(n > 0 ? n : 1));
-    for (int64_t r = 0; r < n; ++r) {
-      c[r].s = orc_b2sp(qc + q * cb, dc + r * cb, d);
-      c[r].id = id_base + r;
-    }
-    qsort(c, (size_t)n, sizeof(orc_cand_t), cmp_cand);
-    for (int32_t j = 0; j < k; ++j) {
-      out_s[q * k + j] = (j < n) ? c[j].s : INT32_MIN;
-      out_id[q * k + j] = (j < n) ? c[j].id : -1;
-    }
-    free(c);
+    for (int64_t q = 0; q < nq; ++q) knn_one(qc + q * cb, dc, n, d, k, id_base, 0, out_s + q * k, out_id + q * k);
+  } else {
+    /* few queries over many rows (full-size sampled checks): rows in parallel */
+    for (int64_t q = 0; q < nq; ++q) knn_one(qc + q * cb, dc, n, d, k, id_base, 1, out_s + q * k, out_id + q * k);
   }
 }
 
@@ -214,23 +236,31 @@ static int32_t masked_add(const int8_t* q, const uint8_t* code, int32_t d) {
   return s;
 }
 
+static void knn_asym_one(const int8_t* q, const uint8_t* dc, int64_t n, int32_t d, int32_t k, int64_t id_base,
+                         int rows_parallel, int32_t* out_s, int64_t* out_id) {
+  const int64_t cb = orc_code_bytes(d);
+  orc_cand_t* c = (orc_cand_t*)malloc(sizeof(orc_cand_t) * (size_t)(n > 0 ? n : 1));
+#pragma omp parallel for schedule(static) if (rows_parallel)
+  for (int64_t r = 0; r < n; ++r) {
+    c[r].s = masked_add(q, dc + r * cb, d);
+    c[r].id = id_base + r;
+  }
+  qsort(c, (size_t)n, sizeof(orc_cand_t), cmp_cand);
+  for (int32_t j = 0; j < k; ++j) {
+    out_s[j] = (j < n) ? c[j].s : INT32_MIN;
+    out_id[j] = (j < n) ? c[j].id : -1;
+  }
+  free(c);
+}
+
 /* Exhaustive kNN by masked addition: order (score desc, id asc), keep k, pad. */
 void orc_knn_asym(const int8_t* q8, int64_t nq, const uint8_t* dc, int64_t n, int32_t d, int32_t k,
                   int64_t id_base, int32_t* out_s, int64_t* out_id) {
-  const int64_t cb = orc_code_bytes(d);
+  if (nq >= orc_threads()) {
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int64_t q = 0; q < nq; ++q) {
-    orc_cand_t* c = (orc_cand_t*)malloc(sizeof(orc_cand_t) * (size_t)(n > 0 ? n : 1));
-    for (int64_t r = 0; r < n; ++r) {
-      c[r].s = masked_add(q8 + q * d, dc + r * cb, d);
-      c[r].id = id_base + r;
-    }
-    qsort(c, (size_t)n, sizeof(orc_cand_t), cmp_cand);
-    for (int32_t j = 0; j < k; ++j) {
-      out_s[q * k + j] = (j < n) ? c[j].s : INT32_MIN;
-      out_id[q * k + j] = (j < n) ? c[j].id : -1;
-    }
-    free(c);
+    for (int64_t q = 0; q < nq; ++q) knn_asym_one(q8 + q * d, dc, n, d, k, id_base, 0, out_s + q * k, out_id + q * k);
+  } else {
+    for (int64_t q = 0; q < nq; ++q) knn_asym_one(q8 + q * d, dc, n, d, k, id_base, 1, out_s + q * k, out_id + q * k);
   }
 }
 

@@ -197,20 +197,28 @@ def search_resolve(nq: int, n: int, d: int, k: int, algo: int = ALGO_AUTO) -> in
     return int(r.value)
 
 
-def build_f4_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
+def build_f4_index(dbcodes: torch.Tensor, d: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """E2M1 index of the database codes for the pair engine (uq_build_f4_index)."""
     _dev(dbcodes, "dbcodes")
     n = dbcodes.shape[0]
-    out = _empty(stream, max(int(_L.uq_f4_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
+    nb = max(int(_L.uq_f4_index_bytes(n, d)), 16)
+    if out is None:
+        out = _empty(stream, nb, dtype=torch.uint8, device=dbcodes.device)
+    elif out.dtype != torch.uint8 or out.numel() != nb or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous uint8 tensor of {nb} bytes")
     _check("uq_build_f4_index", _L.uq_build_f4_index(_ptr(dbcodes), n, d, _ptr(out), _stream(stream)))
     return out
 
 
-def build_i8_index(dbcodes: torch.Tensor, d: int, stream=None) -> torch.Tensor:
+def build_i8_index(dbcodes: torch.Tensor, d: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """int8 index of the database codes for single-operand search (uq_build_i8_index)."""
     _dev(dbcodes, "dbcodes")
     n = dbcodes.shape[0]
-    out = _empty(stream, max(int(_L.uq_i8_index_bytes(n, d)), 16), dtype=torch.uint8, device=dbcodes.device)
+    nb = max(int(_L.uq_i8_index_bytes(n, d)), 16)
+    if out is None:
+        out = _empty(stream, nb, dtype=torch.uint8, device=dbcodes.device)
+    elif out.dtype != torch.uint8 or out.numel() != nb or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous uint8 tensor of {nb} bytes")
     _check("uq_build_i8_index", _L.uq_build_i8_index(_ptr(dbcodes), n, d, _ptr(out), _stream(stream)))
     return out
 

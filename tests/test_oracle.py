@@ -367,3 +367,33 @@ def test_knn_asym_masked_addition(orc):
         assert np.array_equal(ids[r], order) and np.array_equal(s[r], full[r][order])
     s2, i2 = orc.knn_asym(q8, codes[:5], d, 8)   # n < k: padding
     assert (i2[:, 5:] == -1).all() and (s2[:, 5:] == np.iinfo(np.int32).min).all()
+
+
+@pytest.mark.parametrize("threads", [1, 4])
+def test_knn_row_parallel_path(orc, threads):
+    """Few queries (nq < threads) take the row-parallel loop of orc_knn /
+    orc_knn_asym (used by the full-size sampled checks); it must equal the
+    lexsort brute force and the one-query-per-thread path exactly."""
+    prev = orc.set_threads(threads)
+    try:
+        rng = np.random.default_rng(31)
+        d, x, n, k = 160, 80, 5000, 20
+        u = rng.standard_normal((n + 40, d))
+        u[100:110] = u[4000]                        # ties broken by id
+        codes = orc.pack(orc.encode(u, x))
+        db, q = codes[:n], codes[n:]
+        for nq in (1, 3):
+            s, ids = orc.knn(q[:nq], db, d, k, id_base=9)
+            ref_s, ref_i = _np_knn(orc.scores(q[:nq], db, d), k, id_base=9)
+            assert (s == ref_s).all() and (ids == ref_i).all()
+        s_all, i_all = orc.knn(q, db, d, k, id_base=9)   # 40 >= threads: query-parallel path
+        s3, i3 = orc.knn(q[:3], db, d, k, id_base=9)
+        assert (s_all[:3] == s3).all() and (i_all[:3] == i3).all()
+        q8 = orc.quantize_i8(u[n:n + 2].astype(np.float32))
+        sa, ia = orc.knn_asym(q8, db, d, k)
+        full = q8.astype(np.int64) @ orc.unpack(db, d).astype(np.int64).T
+        for r in range(2):
+            order = np.lexsort((np.arange(n), -full[r]))[:k]
+            assert np.array_equal(ia[r], order) and np.array_equal(sa[r], full[r][order])
+    finally:
+        orc.set_threads(prev)
