@@ -78,6 +78,8 @@ def test_rerank_parity(uq, orc, dt, d, n_cand, k):
     fin = np.isfinite(o_s)
     assert np.array_equal(np.isfinite(c), fin)
     assert np.abs(c[fin] - o_s[fin]).max() <= 1e-5
+    big = fin & (np.abs(o_s) >= 0.1)           # north star: 1e-5 relative where the cosine is not tiny
+    assert (np.abs(c[big] - o_s[big]) <= 1e-5 * np.abs(o_s[big])).all()
     sure = _sure_mask(np.where(fin, o_s, -9.0), 2e-5)
     gi = ids.cpu().numpy()
     assert np.array_equal(gi[sure], o_i[sure])
@@ -86,6 +88,33 @@ def test_rerank_parity(uq, orc, dt, d, n_cand, k):
     for r in range(nq):
         v = [x for x in gi[r].tolist() if x >= 0]
         assert len(set(v)) == len(v) and set(v) <= set(cand[r].tolist())
+
+
+@pytest.mark.parametrize("dt,d", [(torch.float32, 768), (torch.float16, 768), (torch.float32, 1536)])
+def test_rerank_parity_mixture_relative(uq, orc, dt, d):
+    """Re-rank on mixture data (BASELINE c2/c4/c5 recipe: candidates are
+    neighbours, cosines ~0.5-0.99): every cosine within 1e-5 RELATIVE of the
+    fp64 oracle (north star), ids equal wherever the fp64 cosines are separated
+    by more than 2e-5 relative, the rest distinct valid candidates."""
+    name = "c4" if d == 1536 else "c2"
+    w = datagen.CONFIGS[name].scaled(n=20_000, nq=24, dtype=dt, centres=200)
+    db = datagen.db(w, "cuda")
+    q = datagen.queries(w, "cuda")
+    o_db = orc.pack(orc.encode(db.float().cpu().numpy(), w.x))
+    o_q = orc.pack(orc.encode(q.float().cpu().numpy(), w.x))
+    _, o_cand = orc.knn(o_q, o_db, w.d, 300)
+    cand = torch.from_numpy(np.ascontiguousarray(o_cand)).cuda()
+    cos, ids = uq.rerank(q, db, cand, 100)
+    o_s, o_i = orc.rerank(q.double().cpu().numpy(), db.double().cpu().numpy(), o_cand, 100)
+    c = cos.double().cpu().numpy()
+    assert (np.abs(o_s) >= 0.1).mean() > 0.99
+    assert (np.abs(c - o_s) <= 1e-5 * np.maximum(np.abs(o_s), 0.1)).all(), np.abs(c - o_s).max()
+    sure = _sure_mask(o_s, 2e-5 * np.abs(o_s).max())
+    gi = ids.cpu().numpy()
+    assert np.array_equal(gi[sure], o_i[sure])
+    for r in range(w.nq):
+        v = gi[r].tolist()
+        assert len(set(v)) == len(v) and set(v) <= set(o_cand[r].tolist())
 
 
 def test_rerank_after_search_is_k_at_n(uq, orc):
