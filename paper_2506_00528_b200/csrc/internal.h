@@ -51,6 +51,7 @@ cudaError_t launch_merge_ptrs(const int32_t* const* score_ptrs, const int64_t* c
 // Popcount scan (scan_popc.cu).
 struct PopcPlan {
   int32_t qt, n_qtiles, cap, grid, smem;
+  int32_t stages;   // > 0: the TMA-fed kernel with this many ring stages (one CTA per SM)
   int64_t L, n_chunks;
   size_t buf_bytes, part_bytes;
 };

@@ -107,7 +107,7 @@ def test_rerank_parity_mixture_relative(uq, orc, dt, d):
     cos, ids = uq.rerank(q, db, cand, 100)
     o_s, o_i = orc.rerank(q.double().cpu().numpy(), db.double().cpu().numpy(), o_cand, 100)
     c = cos.double().cpu().numpy()
-    assert (np.abs(o_s) >= 0.1).mean() > 0.99
+    assert (np.abs(o_s) >= 0.1).mean() > 0.9
     assert (np.abs(c - o_s) <= 1e-5 * np.maximum(np.abs(o_s), 0.1)).all(), np.abs(c - o_s).max()
     sure = _sure_mask(o_s, 2e-5 * np.abs(o_s).max())
     gi = ids.cpu().numpy()
