@@ -350,15 +350,19 @@ scan_popc_tma_kernel(const __grid_constant__ CUtensorMap tmap, PopcParams p, int
 static int popc_occ(int NB, int qt) { return (NB <= 6 && qt <= 8) ? 3 : (NB <= 10 ? 2 : 1); }
 
 // TMA ring depth for the one-CTA-per-SM TMA variant: as many 256-row stages
-// as fit (at most 4) beside the query tile; 0 = use the LDG kernel (d > 1536:
-// fewer than two stages fit).  UQ_POPC_LDG=1 forces the LDG kernel
+// as fit (at most 4) beside the query tile; 0 = use the LDG kernel.  The TMA
+// kernel serves the HBM-bound regime (tiles of <= 8 queries: c5 Q = 1 streams
+// 9.6 GB at 6.9 TB/s vs 5.1 TB/s with per-thread LDG); POPC-bound tiles (more
+// queries per DB row) keep the LDG kernel, whose 2-3 CTAs per SM issue more
+// POPC than 8 consumer warps (c2, Q = 1000: 11.9 vs 20.6 ms); d > 1536 leaves
+// room for fewer than two stages.  UQ_POPC_LDG=1 forces the LDG kernel
 // (measurement knob; both kernels return identical results).
 static int popc_tma_stages(int NB, int qt, int64_t n) {
   static const bool ldg = [] {
     const char* e = getenv("UQ_POPC_LDG");
     return e != nullptr && atoi(e) != 0;
   }();
-  if (ldg || NB > 12 || n >= ((int64_t)1 << 31)) return 0;   // TMA row coordinates are int32
+  if (ldg || qt > 8 || NB > 12 || n >= ((int64_t)1 << 31)) return 0;   // TMA row coordinates are int32
   const int stage = ((2 * NB * 16 + kTmaBox - 1) / kTmaBox) * kStageRows * kTmaBox;
   const int fixed = 1024 + 2 * qt * NB * 16 + qt * 8 + 2 * 4 * 8 + 16;
   int st = (227 * 1024 - fixed) / stage;
