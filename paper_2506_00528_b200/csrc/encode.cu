@@ -20,6 +20,11 @@
 //      every third pass a key-space bisection, so the key range at least halves
 //      every three passes and the search ends in <= 3*31 passes whatever the
 //      data), until count(>= c) == x or hi == lo + 1.
+// f32 runs steps 1-2 first on COARSE keys -- the top 16 bits of two keys per
+// word (a bf16 truncation), compared as f16 patterns by HSET2 and counted by
+// HADD2, half the instructions of a 32-bit key pass; coarse(a) > coarse(b)
+// implies key(a) > key(b), so the coarse bracket is a key bracket -- and only
+// the last one-coarse-value bracket (a few keys) with full 32-bit keys.
 // The probes only steer the search: T* is exact for any input.  fp16 rows count
 // two keys per instruction (HSET2 on |u| half pairs, exact small-integer HADD2).
 // Keys > T* are selected, keys == T* are taken in index order until x are
@@ -29,6 +34,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -62,7 +68,6 @@ template <> struct ElemBits<__nv_bfloat16> {
 };
 
 constexpr int kEncWarps = 8;
-constexpr float kProbeDelta = 0.08f;
 constexpr int kMaxCodeBytes = 2 * 16 * ((UQ_MAX_D + 127) / 128);
 
 // element c of a raw 16-byte word as its IEEE bit pattern
@@ -168,6 +173,45 @@ struct Counter<__half, E, NCH> {
 
 #define KEY(e) raw_elem<T>(raw[(e) / VEC], (e) % VEC)
 
+__device__ __forceinline__ __half2 as_h2(uint32_t w) { return *reinterpret_cast<const __half2*>(&w); }
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<const uint32_t*>(&h); }
+
+// 1/v (MUFU.RCP; steering arithmetic only, never decides a bit)
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// f32 coarse keys (two 15-bit patterns per word, compared as f16): count >= c
+template <int NW>
+__device__ __forceinline__ unsigned coarse_ge(const uint32_t (&cw)[NW], uint32_t c) {
+  const __half2 cc = as_h2(c | (c << 16));
+  __half2 a0 = __float2half2_rn(0.f), a1 = a0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    const __half2 w = as_h2(cw[i]);
+    if (i & 1) a1 = __hadd2(a1, __hge2(w, cc));
+    else a0 = __hadd2(a0, __hge2(w, cc));
+  }
+  const __half2 a = __hadd2(a0, a1);
+  return (unsigned)(__low2float(a) + __high2float(a));
+}
+template <int NW>
+__device__ __forceinline__ void coarse_ge2(const uint32_t (&cw)[NW], uint32_t c1, uint32_t c2, unsigned& n1,
+                                           unsigned& n2) {
+  const __half2 cc1 = as_h2(c1 | (c1 << 16)), cc2 = as_h2(c2 | (c2 << 16));
+  __half2 a1 = __float2half2_rn(0.f), a2 = a1;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    const __half2 w = as_h2(cw[i]);
+    a1 = __hadd2(a1, __hge2(w, cc1));
+    a2 = __hadd2(a2, __hge2(w, cc2));
+  }
+  n1 = (unsigned)(__low2float(a1) + __high2float(a1));
+  n2 = (unsigned)(__low2float(a2) + __high2float(a2));
+}
+
 // Four words of 16-bit lanes with flags in bits 15 and 31 -> 8 bits, bit
 // 2i + h = flag of half h of word i (PRMT gathers the flag bytes, one multiply
 // moves bits 7/15/23/31 to 28..31 without carries).
@@ -178,16 +222,16 @@ __device__ __forceinline__ uint32_t flags16_to_bits8(uint32_t w0, uint32_t w1, u
   const uint32_t n23 = ((t23 & 0x80808080u) * 0x00204081u) >> 28;
   return n01 | (n23 << 4);
 }
-__device__ __forceinline__ __half2 as_h2(uint32_t w) { return *reinterpret_cast<const __half2*>(&w); }
-
 // NCH: chunks of 32*VEC elements per row (compile-time so keys live in registers).
 template <typename T, int NCH, bool VECLOAD>
-__global__ void __launch_bounds__(kEncWarps * 32)
-encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t x, float z0,
+__global__ void __launch_bounds__(kEncWarps * 32, (sizeof(T) == 4 && NCH > 8) ? 2 : 3)
+encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t x, float z0, float delta,
               uint8_t* __restrict__ codes) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int E = NCH * VEC;        // elements per lane
-  constexpr int NS = (sizeof(T) == 4) ? NCH : (NCH < 2 ? NCH : 2);  // chunks used for the RMS
+  constexpr int NS = (sizeof(T) == 4) ? (NCH < 2 ? NCH : NCH / 2) : (NCH < 2 ? NCH : 2);  // chunks used for the RMS
+  constexpr bool F32 = sizeof(T) == 4;
+  constexpr int NWC = F32 ? E / 2 : 1;   // f32: coarse words (top 16 bits of two keys each)
   using EB = ElemBits<T>;
   using CNT = Counter<T, E, NCH>;
   const int lane = threadIdx.x & 31;
@@ -238,22 +282,40 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
         raw[j].x &= 0x7fff7fffu; raw[j].y &= 0x7fff7fffu; raw[j].z &= 0x7fff7fffu; raw[j].w &= 0x7fff7fffu;
       }
       ss = (__low2float(acc) + __high2float(acc)) * 4096.f;
-    } else {
+    } else if constexpr (!F32) {
+      // bf16: sign flags as f16 (bits 15/31 of each word); RMS from the halves widened to f32
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
+        sgnm |= (uint64_t)flags16_to_bits8(raw[j].x, raw[j].y, raw[j].z, raw[j].w) << (8 * j);
+        if (j < NS) {
+          const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
 #pragma unroll
-        for (int c = 0; c < VEC; ++c) {
-          const uint32_t r = raw_elem<T>(raw[j], c);
-          const int e = j * VEC + c;
-          if (EB::sign(r)) sgnm |= 1ull << e;
-          if (j < NS) {
-            const float v = EB::key2f(EB::abs_bits(r));
-            ss = fmaf(v, v, ss);
+          for (int i = 0; i < 4; ++i) {
+            const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
+            ss = fmaf(lo, lo, fmaf(hi, hi, ss));
           }
         }
-        // keys in place: clear the sign bits
-        constexpr uint32_t m = (sizeof(T) == 4) ? 0x7fffffffu : 0x7fff7fffu;
-        raw[j].x &= m; raw[j].y &= m; raw[j].z &= m; raw[j].w &= m;
+        raw[j].x &= 0x7fff7fffu; raw[j].y &= 0x7fff7fffu; raw[j].z &= 0x7fff7fffu; raw[j].w &= 0x7fff7fffu;
+      }
+    } else {
+      // f32: sign bits shifted in by funnel shifts (one SHF per element, last
+      // element first so that bit e ends up at position e)
+      uint32_t sg[2] = {0u, 0u};
+#pragma unroll
+      for (int e = E - 1; e >= 0; --e) {
+        const uint32_t r = raw_elem<T>(raw[e / VEC], e % VEC);
+        sg[e >> 5] = __funnelshift_l(r, sg[e >> 5], 1);
+      }
+      sgnm = (uint64_t)sg[0] | ((uint64_t)sg[1] << 32);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        if (j < NS) {
+          ss = fmaf(__uint_as_float(raw[j].x), __uint_as_float(raw[j].x), ss);
+          ss = fmaf(__uint_as_float(raw[j].y), __uint_as_float(raw[j].y), ss);
+          ss = fmaf(__uint_as_float(raw[j].z), __uint_as_float(raw[j].z), ss);
+          ss = fmaf(__uint_as_float(raw[j].w), __uint_as_float(raw[j].w), ss);
+        }
+        raw[j].x &= 0x7fffffffu; raw[j].y &= 0x7fffffffu; raw[j].z &= 0x7fffffffu; raw[j].w &= 0x7fffffffu;
       }
     }
 #pragma unroll
@@ -271,9 +333,65 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
       else if (cnt > (unsigned)x) { if (c > lo) { lo = c; clo = cnt; } }
       else if (c < hi) { hi = c; chi = cnt; }
     };
-    {
+    if constexpr (F32) {
+      // Coarse phase: the top 16 bits of two keys per word (a bf16 truncation),
+      // compared as f16 patterns (for non-negative patterns the f16 order is the
+      // integer order; >= 0x7C00 -- |u| >= 2^121 -- clamped to 0x7BFF by HMNMX2),
+      // counted two keys per HSET2 + HADD2: half the cost of a full-key pass.
+      // coarse(a) > coarse(b) => key(a) > key(b), so the coarse bracket is a key
+      // bracket: [lo_c << 16, hi_c << 16).  It ends exact (exactly x keys have
+      // coarse >= Tc, i.e. key >= Tc << 16) or one coarse value wide (its few
+      // keys are then resolved by full-key passes below).
+      uint32_t cw[NWC];
+      const __half2 cmax = as_h2(0x7bff7bffu);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        cw[2 * j] = h2_bits(__hmin2(as_h2(__byte_perm(raw[j].x, raw[j].y, 0x7632)), cmax));
+        cw[2 * j + 1] = h2_bits(__hmin2(as_h2(__byte_perm(raw[j].z, raw[j].w, 0x7632)), cmax));
+      }
+      uint32_t lc = 0u, hc = 0x7c00u;
       const float t = rms * ratio;
-      uint32_t p1 = EB::f2key(t * (1.f - kProbeDelta)), p2 = EB::f2key(t * (1.f + kProbeDelta));
+      uint32_t p1 = (__float_as_uint(t * (1.f - delta)) >> 16) & 0x7fffu;
+      uint32_t p2 = (__float_as_uint(t * (1.f + delta)) >> 16) & 0x7fffu;
+      p1 = min(max(p1, 1u), 0x7bfeu);
+      p2 = min(max(p2, p1 + 1u), 0x7bffu);
+      unsigned n1, n2;
+      coarse_ge2<NWC>(cw, p1, p2, n1, n2);
+      n1 = __reduce_add_sync(kFull, n1);
+      n2 = __reduce_add_sync(kFull, n2);
+      auto cupd = [&](uint32_t c, unsigned cnt) {
+        if (exact) return;
+        if (cnt == (unsigned)x) { Tk = c << 16; exact = true; }
+        else if (cnt > (unsigned)x) { if (c > lc) { lc = c; clo = cnt; } }
+        else if (c < hc) { hc = c; chi = cnt; }
+      };
+      cupd(p1, n1);
+      cupd(p2, n2);
+      unsigned cph = 0;
+#pragma unroll 1
+      while (!exact && hc - lc > 1u) {
+        const float vl = __uint_as_float(lc << 16), vh = __uint_as_float(hc << 16);
+        const float f = ((float)(clo - (unsigned)x) + 0.5f) * rcp_approx((float)(clo - chi));
+        const uint32_t ci = min(max((__float_as_uint(fmaf(f, vh - vl, vl)) >> 16) & 0x7fffu, lc + 1u), hc - 1u);
+        const bool bis = (hc == 0x7c00u) || cph == 2u;
+        cph = (cph == 2u) ? 0u : cph + 1u;
+        const uint32_t c = bis ? lc + ((hc - lc) >> 1) : ci;
+        const unsigned cnt = __reduce_add_sync(kFull, coarse_ge<NWC>(cw, c));
+        exact = cnt == (unsigned)x;
+        const bool up = cnt > (unsigned)x;
+        Tk = c << 16;
+        lc = up ? c : lc;
+        clo = up ? cnt : clo;
+        hc = up ? hc : c;
+        chi = up ? chi : cnt;
+      }
+      // full-key bracket (the clamped top coarse value reaches the end of the key range)
+      lo = lc << 16;
+      hi = (hc == 0x7c00u) ? EB::kKeyEnd : (hc << 16);
+      if (hc == 0x7c00u) chi = 0u;
+    } else {
+      const float t = rms * ratio;
+      uint32_t p1 = EB::f2key(t * (1.f - delta)), p2 = EB::f2key(t * (1.f + delta));
       p1 = min(max(p1, 1u), EB::kKeyEnd - 2u);
       p2 = min(max(p2, p1 + 1u), EB::kKeyEnd - 1u);
       unsigned n1, n2;
@@ -287,7 +405,7 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
 #pragma unroll 1
     while (!exact && hi - lo > 1u) {
       const float vl = EB::key2f(lo), vh = EB::key2f(hi);
-      const float f = __fdividef((float)(clo - (unsigned)x) + 0.5f, (float)(clo - chi));
+      const float f = ((float)(clo - (unsigned)x) + 0.5f) * rcp_approx((float)(clo - chi));
       const uint32_t ci = min(max(EB::f2key(fmaf(f, vh - vl, vl)), lo + 1u), hi - 1u);
       const bool bis = (hi == EB::kKeyEnd) || phase == 2u;
       phase = (phase == 2u) ? 0u : phase + 1u;
@@ -322,6 +440,12 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
           selm |= (uint64_t)flags16_to_bits8(__hge2_mask(as_h2(raw[j].x), t2), __hge2_mask(as_h2(raw[j].y), t2),
                                              __hge2_mask(as_h2(raw[j].z), t2), __hge2_mask(as_h2(raw[j].w), t2))
                   << (8 * j);
+      } else if constexpr (F32) {
+        // bit = (key >= lo_sel) = sign of (lo_sel - 1 - key) (both < 2^31), shifted in
+        uint32_t sl[2] = {0u, 0u};
+#pragma unroll
+        for (int e = E - 1; e >= 0; --e) sl[e >> 5] = __funnelshift_l(lo_sel - 1u - KEY(e), sl[e >> 5], 1);
+        selm = (uint64_t)sl[0] | ((uint64_t)sl[1] << 32);
       } else {
 #pragma unroll
         for (int e = 0; e < E; ++e)
@@ -443,12 +567,22 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
   // |u|_(x) of d i.i.d. N(0, s^2) draws ~ s * Phi^-1(1 - x / 2d)
   float z0 = inv_norm_cdf(1.0 - ((double)x - 0.5) / (2.0 * (double)d));
   if (!(z0 > 1e-3f)) z0 = 1e-3f;
+  // probe half-width: the probes bracket T* unless the predicted T* / RMS
+  // ratio is off by more than delta (steering only; UQ_ENC_DELTA overrides).
+  // Measured optimum (tools/enc_bench.py over delta in 0.02-0.30,
+  // profiles/r02/enc_delta_scan.txt): 0.12 for f32 (coarse phase), 0.08 for
+  // 16-bit keys.
+  static const float delta_env = [] {
+    const char* e = getenv("UQ_ENC_DELTA");
+    return e ? (float)atof(e) : 0.f;
+  }();
+  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.12f : 0.08f);
   if (vec)
     encode_kernel<T, NCH, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-        (const T*)u, n, d, ld, x, z0, codes);
+        (const T*)u, n, d, ld, x, z0, delta, codes);
   else
     encode_kernel<T, NCH, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-        (const T*)u, n, d, ld, x, z0, codes);
+        (const T*)u, n, d, ld, x, z0, delta, codes);
   note_launch();
   return cudaGetLastError();
 }
