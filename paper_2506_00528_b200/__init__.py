@@ -22,9 +22,11 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# tools/ may load the profile build (timing ablations compiled in) by setting
-# UQ_PROFILE_LIB=1 before import; everything else loads the product library.
-_LIB_PATH = os.path.join(_HERE, "libuq_prof.so" if os.environ.get("UQ_PROFILE_LIB") == "1" else "libuq.so")
+# tools/ may load the profile build (timing ablations compiled in) with
+# UQ_PROFILE_LIB=1, or the checked build (device bounds asserts) with
+# UQ_CHECKED_LIB=1, set before import; everything else loads the product library.
+_LIB_PATH = os.path.join(_HERE, "libuq_prof.so" if os.environ.get("UQ_PROFILE_LIB") == "1" else
+                         "libuq_checked.so" if os.environ.get("UQ_CHECKED_LIB") == "1" else "libuq.so")
 
 ALGO_AUTO, ALGO_POPC, ALGO_TCGEN05, ALGO_TC_FP4 = 0, 1, 2, 3
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}

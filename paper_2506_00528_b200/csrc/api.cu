@@ -234,7 +234,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
                                   uint64_t* part, int32_t* part_cnt, int32_t* out_s, int64_t* out_id, int sms,
                                   int timer_kind, cudaStream_t st, const int32_t* qfail = nullptr,
                                   const int32_t* any = nullptr, void* mscr = nullptr, size_t mscr_bytes = 0,
-                                  const uint8_t* dbx = nullptr) {
+                                  const uint8_t* dbx = nullptr, size_t dbx_bytes = 0) {
   cudaEvent_t ev;
   int64_t lists = 0;
   cudaError_t e;
@@ -243,7 +243,7 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
   if (is_tc(a)) {
     const TcPlan tp = plan_tc_for(a, nq, n, d, k, sms);
     e = op >= 0 ? launch_scan_tc2(q, nq, db, n, d, k, tp, bufs, part, part_cnt, thr0, thr0_stride, row_stride, op, st,
-                                  qfail, any, nullptr, 0, dbx)
+                                  qfail, any, nullptr, 0, dbx, dbx_bytes)
                 : launch_scan_tc(q, nq, db, n, d, k, tp, bufs, part, thr0, thr0_stride, row_stride, st);
     lists = tp.n_chunks;
   } else {
@@ -404,6 +404,7 @@ static uq_status search_impl(const uint8_t* qcodes, int64_t nq, const uint8_t* d
   const int32_t* thr0 = nullptr;
   int32_t thr0_stride = k;
   const int32_t need = (sp.on && hist) ? seed_need(k, sp.stride) : k;
+  const size_t dbx_bytes = dbx != nullptr ? f4_index_bytes(n, d) : 0;   // uq_search_f4x checked the caller's size
   if (sp.on && hist) {
     // Delta histogram of a strided sample -> per-query bound on D_k
     int32_t* thr = reinterpret_cast<int32_t*>(ws + L.seed_s_off);
@@ -413,7 +414,7 @@ static uq_status search_impl(const uint8_t* qcodes, int64_t nq, const uint8_t* d
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)sp.rows);
     cudaError_t e = launch_seed_tc2_hist(qcodes, nq, dbcodes, sp.rows, d, k, need, sp.stride, ghist, qbase, thr,
-                                         sms, pair_op(a, nq, d), st, nullptr, 0, dbx);
+                                         sms, pair_op(a, nq, d), st, nullptr, 0, dbx, dbx_bytes);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = thr;
@@ -430,7 +431,7 @@ static uq_status search_impl(const uint8_t* qcodes, int64_t nq, const uint8_t* d
   // main scan: a row can enter query q's streams only if Delta >= seed D_k(q)
   cudaError_t e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, thr0, thr0_stride, bufs, part,
                                  part_cnt, out_scores, out_ids, sms, 0, st, nullptr, nullptr, ws + L.mscr_off,
-                                 L.mscr_bytes, dbx);
+                                 L.mscr_bytes, dbx, dbx_bytes);
   if (e != cudaSuccess || !(sp.on && hist && need < k)) return from_cuda(e);
   // optimistic seeds: queries with fewer than k rows above their bound are
   // searched again without one (device-side flags: no host round trip; the
@@ -441,7 +442,7 @@ static uq_status search_impl(const uint8_t* qcodes, int64_t nq, const uint8_t* d
   e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = scan_and_merge(a, qcodes, nq, dbcodes, n, d, k, id_base, 1, nullptr, 0, bufs, part, part_cnt, out_scores,
-                     out_ids, sms, -1, st, fail, any, ws + L.mscr_off, L.mscr_bytes, dbx);
+                     out_ids, sms, -1, st, fail, any, ws + L.mscr_off, L.mscr_bytes, dbx, dbx_bytes);
   return from_cuda(e);
 }
 
@@ -599,6 +600,7 @@ static uq_status asym_impl(const int8_t* q8, int64_t nq, int64_t ldq, const uint
   int32_t* cnt = reinterpret_cast<int32_t*>(ws + L.cnt_off);
   int32_t* thr = reinterpret_cast<int32_t*>(ws + L.thr_off);
   const int32_t* thr0 = nullptr;
+  const size_t dbx_bytes = dbx != nullptr ? i8_index_bytes(n, d) : 0;   // uq_search_asym_x checked the caller's size
   cudaError_t e;
   if (L.sp.on) {
     uint32_t* ghist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
@@ -607,7 +609,7 @@ static uq_status asym_impl(const int8_t* q8, int64_t nq, int64_t ldq, const uint
     cudaEvent_t ev;
     timer_begin(st, &ev, 1, (double)nq * (double)L.sp.rows);
     e = launch_seed_tc2_hist(nullptr, nq, dbcodes, L.sp.rows, d, k, L.need, L.sp.stride, ghist, qbase, thr, sms, 0,
-                             st, q8, ldq, dbx);
+                             st, q8, ldq, dbx, dbx_bytes);
     timer_end(st, ev);
     if (e != cudaSuccess) return UQ_ERR_CUDA;
     thr0 = thr;
@@ -615,7 +617,7 @@ static uq_status asym_impl(const int8_t* q8, int64_t nq, int64_t ldq, const uint
   cudaEvent_t ev;
   timer_begin(st, &ev, 0, (double)nq * (double)n);
   e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, thr0, 1, 1, 0, st, nullptr, nullptr,
-                      q8, ldq, dbx);
+                      q8, ldq, dbx, dbx_bytes);
   timer_end(st, ev);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st, cnt, nullptr,
@@ -628,7 +630,7 @@ static uq_status asym_impl(const int8_t* q8, int64_t nq, int64_t ldq, const uint
   e = launch_seed_verify(out_ids, nq, k, thr0, fail, any, st);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   e = launch_scan_tc2(nullptr, nq, dbcodes, n, d, k, L.main, bufs, part, cnt, nullptr, 0, 1, 0, st, fail, any, q8,
-                      ldq, dbx);
+                      ldq, dbx, dbx_bytes);
   if (e != cudaSuccess) return UQ_ERR_CUDA;
   return from_cuda(launch_merge_keys(part, L.main.n_chunks, nq, L.main.cap, k, id_base, out_scores, out_ids, st,
                                      cnt, fail, any, ws + L.mscr_off, L.mscr_bytes));

@@ -7,6 +7,28 @@
 
 #include "../../include/uq.h"
 
+// Device-side bounds checks of the CHECKED build (libuq_checked.so, built
+// with -DUQ_CHECKED by `build.py --checked`; tools/sanitize.py runs every
+// engine against it).  compute-sanitizer is not available on the GPU pool, so
+// these asserts stand in for its memcheck on the accesses that matter: stream
+// buffer appends, candidate-list writes, bulk-copy sources inside the index,
+// shared-memory code buffers.  The product library compiles them out.
+#ifdef UQ_CHECKED
+#include <cstdio>
+#define UQ_ASSERT(c)                                                                 \
+  do {                                                                               \
+    if (!(c)) {                                                                      \
+      printf("UQ_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                     \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define UQ_ASSERT(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace uq {
 
 constexpr int kWarp = 32;
@@ -181,6 +203,7 @@ __device__ uint32_t ordered_rebuild_regs(uint32_t* buf, int cnt, int k, int lane
 
 #define UQ_REBUILD_DISPATCH(FN, ...)                          \
   do {                                                        \
+    UQ_ASSERT(cnt <= 48 * kWarp);                             \
     if (cnt <= 8 * kWarp) return FN<8>(__VA_ARGS__);          \
     if (cnt <= 16 * kWarp) return FN<16>(__VA_ARGS__);        \
     if (cnt <= 24 * kWarp) return FN<24>(__VA_ARGS__);        \

@@ -507,6 +507,7 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
         byte_idx = (uint32_t)j * 32u + (uint32_t)lane;
         wr = true;
       }
+      UQ_ASSERT(!wr || byte_idx >= (uint32_t)(pw * 4) || pw * 8 <= kMaxCodeBytes);
       if (wr && byte_idx < (uint32_t)(pw * 4)) {
         s_code[byte_idx] = (uint8_t)v;
         s_code[pw * 4 + byte_idx] = (uint8_t)(v >> 8);

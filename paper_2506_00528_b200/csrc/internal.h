@@ -89,7 +89,7 @@ TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int o
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
                                  int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8 = nullptr,
-                                 int64_t ldq8 = 0, const uint8_t* dbx = nullptr);
+                                 int64_t ldq8 = 0, const uint8_t* dbx = nullptr, size_t dbx_bytes = 0);
 // After a search with optimistic seeds: fail[q] = 1 iff q was filtered
 // (thr[q] != INT32_MIN) and fewer than k rows passed (its k-th result is
 // padding); *any |= 1 if some query failed (*any must be zero on entry).
@@ -101,7 +101,8 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st, const int32_t* qfail = nullptr, const int32_t* any_fail = nullptr,
-                            const int8_t* q8 = nullptr, int64_t ldq8 = 0, const uint8_t* dbx = nullptr);
+                            const int8_t* q8 = nullptr, int64_t ldq8 = 0, const uint8_t* dbx = nullptr,
+                            size_t dbx_bytes = 0);
 // E2M1 index (uq_build_f4_index): rows padded to whole 240-row pair tiles
 size_t f4_index_bytes(int64_t n, int32_t d);
 size_t i8_index_bytes(int64_t n, int32_t d);

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
       for (int64_t l = warp; l < p.lists; l += kMergeWarps) {
         const int o = s_off[l], c = s_off[l + 1] - o;
         const uint64_t* src = p.keys + ((size_t)l * p.nq + q) * p.kin;
+        UQ_ASSERT(o + c <= p.stage_cap);
         for (int e = lane; e < c; e += 32) s_cand[o + e] = src[e];
       }
       C = total;

@@ -88,6 +88,7 @@ __device__ __forceinline__ void popc_stage_queries(const PopcParams& p, const ui
       int base = 0;
       if (lane == 0) base = atomicAdd(&s_cnt[j], __popc(bal));
       base = __shfl_sync(kFull, base, 0);
+      UQ_ASSERT(!pass || base + __popc(bal) <= p.cap);
       if (pass) mybufs[(size_t)j * p.cap + base + __popc(bal & lanemask_lt())] = key;
     }
   }

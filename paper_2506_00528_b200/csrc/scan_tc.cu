@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1) scan_tc_kernel(Params p)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                   const int sc = (int)v[4 * i + j];
+                  UQ_ASSERT(!(sc > thrd) || cnt < p.cap);
                   if (sc > thrd) my_buf[cnt++] = local_key(p.kf, sc, rb0 + (uint32_t)(4 * i + j));
                 }
               }

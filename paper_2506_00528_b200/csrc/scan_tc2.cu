@@ -131,6 +131,7 @@ struct Params {
   const int8_t* q8;     // optional (int8 engine): int8 queries [nq][ldq8] instead of ternary codes
   int64_t ldq8;
   const uint8_t* dbx;   // optional (E2M1 engine): pre-expanded index (uq_build_f4_index), stages by bulk copy
+  size_t dbx_bytes;     // its size (checked builds assert every bulk copy lies inside it; 0 = unknown)
   int32_t dbg;          // timing ablation (env UQ_TC_ABLATE): 1 no expansion, 2 no epilogue work, 4 no DB loads,
                         // 8 cycle accounting, 16 no producer proxy fence
 };
@@ -368,6 +369,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           for (int ks = 0; ks < NST; ++ks) {
             const int nb = (ks + 1) * kBlkPerStage <= NB ? kBlkPerStage : NB - ks * kBlkPerStage;
             const uint32_t bytes = (uint32_t)nb * G::CPB * BH * 16;
+            UQ_ASSERT(p.dbx_bytes == 0 || (size_t)half_tile(tile) * kHalfTileBytes +
+                                              (size_t)ks * kBlkPerStage * G::CPB * BH * 16 + bytes <= p.dbx_bytes);
             mbar_wait(smem_u32(&empty[stage]), sphase ^ 1u);
             const uint32_t bar = smem_u32(&loaded[stage]);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -747,6 +750,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                     const int sc = (int)v[4 * i + j];
                     if (sc > thb) {
                       const int dv = OP != kOpF4 ? sc : raw ? __float2int_rn(__int_as_float(sc)) : sc - kF4Bias;
+                      UQ_ASSERT(cnt < p.cap);
                       my_buf[cnt++] = local_key(p.kf, dv, rb0 + (uint32_t)(4 * i + j));
                       ++n_app;
                     }
@@ -816,6 +820,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
               const size_t list = (size_t)(it.c * kEpiSets + h) * p.nq + qi;
               uint64_t* out = p.part + list * p.cap;
               const int cv = cLs[u];
+              UQ_ASSERT(cv <= p.cap && it.c < p.s_max);
               if (i0 == 0 && lane == 0) p.part_cnt[list] = cv;   // entries past it are never read
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
@@ -1153,14 +1158,15 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
                             int32_t k, const TcPlan& pl, uint32_t* bufs, uint64_t* part, int32_t* part_cnt,
                             const int32_t* thr0, int32_t thr0_stride, int64_t row_stride, int op,
                             cudaStream_t st, const int32_t* qfail, const int32_t* any_fail, const int8_t* q8,
-                            int64_t ldq8, const uint8_t* dbx) {
+                            int64_t ldq8, const uint8_t* dbx, size_t dbx_bytes) {
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   // an index is read by whole contiguous half tiles: top-k scans of an
   // index are over every row (strided top-k scans only seed the other engines)
   if (dbx != nullptr && row_stride != 1) return cudaErrorInvalidValue;
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(q8 ? 127 * d : d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, bufs, part, part_cnt, thr0,
-                thr0_stride, row_stride, nullptr, 0.f, nullptr, 0.f, qfail, any_fail, q8, ldq8, dbx, tc2_dbg()};
+                thr0_stride, row_stride, nullptr, 0.f, nullptr, 0.f, qfail, any_fail, q8, ldq8, dbx, dbx_bytes,
+                tc2_dbg()};
   return launch_tc2_mode<tc2::kModeTopK>(p, pl, blocks128(d), op, st);
 }
 
@@ -1170,7 +1176,7 @@ cudaError_t launch_scan_tc2(const uint8_t* q, int64_t nq, const uint8_t* db, int
 cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                                  int32_t k, int32_t need, int64_t row_stride, uint32_t* ghist, uint32_t* qbase,
                                  int32_t* thr, int sms, int op, cudaStream_t st, const int8_t* q8, int64_t ldq8,
-                                 const uint8_t* dbx) {
+                                 const uint8_t* dbx, size_t dbx_bytes) {
   if (q8 != nullptr && op != tc2::kOpI8) return cudaErrorInvalidValue;
   const TcPlan pl = plan_tc2_hist(nq, n, d, k, sms, op);
   if (!pl.ok) return cudaErrorInvalidValue;
@@ -1186,7 +1192,8 @@ cudaError_t launch_seed_tc2_hist(const uint8_t* q, int64_t nq, const uint8_t* db
   z = z < 0.f ? 0.f : (z > 4.f ? 4.f : z);
   tc2::Params p{q, nq, db, n, d, k, make_keyfmt(d), pl.n_qtiles, pl.s_lo, pl.r_hi,
                 (int32_t)(pl.s_lo + (pl.r_hi > 0 ? 1 : 0)), pl.n_items, pl.cap, pl.stages, nullptr, nullptr, nullptr,
-                nullptr, 0, row_stride, ghist, z, qbase, topsig, nullptr, nullptr, q8, ldq8, dbx, tc2_dbg()};
+                nullptr, 0, row_stride, ghist, z, qbase, topsig, nullptr, nullptr, q8, ldq8, dbx, dbx_bytes,
+                tc2_dbg()};
   cudaError_t e = launch_tc2_mode<tc2::kModeHist>(p, pl, blocks128(d), op, st);
   if (e != cudaSuccess) return e;
   tc2::thr_from_hist_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(ghist, nq, need, qbase, thr);

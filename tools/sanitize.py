@@ -1,7 +1,13 @@
-"""Small (c1-sized) run of every kernel of libuq.so, for compute-sanitizer
-(memcheck / racecheck / synccheck / initcheck; profiles/r02/sanitizer_*.txt):
+"""Small (c1-sized) run of every kernel of libuq.so against the CHECKED build
+(libuq_checked.so: device-side bounds asserts, UQ_ASSERT in csrc/common.cuh),
+every result compared with the CPU oracle:
 
-    compute-sanitizer --tool memcheck python tools/sanitize.py
+    python tools/sanitize.py            # builds + loads libuq_checked.so
+
+compute-sanitizer is closed on this GPU pool (runs under it have left GPUs
+needing a reset; profiles/r02/compute_sanitizer_closed.txt), so the checked
+build's asserts + oracle comparison stand in for its memcheck.  The same
+script runs under compute-sanitizer where that is allowed.
 
 Engines: encode (f32 / f16 / bf16), scores, check_codes, the popcount scan (TMA
 and LDG variants, seeded), the one-CTA int8 tcgen05 scan, the CTA-pair int8 and
@@ -12,6 +18,14 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("UQ_CHECKED_LIB", "1") == "1":
+    os.environ["UQ_CHECKED_LIB"] = "1"
+    import importlib.util as _ilu  # noqa: E402
+    _spec = _ilu.spec_from_file_location("_uqb", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(
+        __file__))), "paper_2506_00528_b200", "build.py"))
+    _m = _ilu.module_from_spec(_spec)
+    _spec.loader.exec_module(_m)
+    _m.build(checked=True)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -82,7 +96,7 @@ def main():
     assert np.abs(cos.double().cpu().numpy() - o_cos).max() <= 1e-5
     print(f"{'rerank':28s} ok", flush=True)
     torch.cuda.synchronize()
-    print("SANITIZE RUN DONE", flush=True)
+    print("SANITIZE RUN DONE:", uq.lib_path(), flush=True)
 
 
 if __name__ == "__main__":
