@@ -132,13 +132,23 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def _dist():
+def _dist(backend: str = "nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if torch.cuda.is_available():
-        torch.cuda.set_device(local)   # before NCCL binds this rank to a device
+        # before NCCL binds this rank to a device; the gloo test mode (below)
+        # lets several ranks share the devices there are
+        local = local % torch.cuda.device_count() if backend == "gloo" else local
+        torch.cuda.set_device(local)
     if world > 1 and not dist.is_initialized():
+        if backend == "gloo":
+            # test mode (tests/test_bench_dist.py): the bench's N > 1 code path
+            # -- shards, global ids, exchange, merge, digest, max-over-ranks
+            # timing -- on one GPU, the lists exchanged through host memory;
+            # the ranks' kernels never wait on each other.  Not a scaling run.
+            dist.init_process_group("gloo")
+            return world, rank, local
         if torch.cuda.is_available() and "NCCL_DEBUG" not in os.environ:
             # NCCL's own record of the communicator (rank count, NVLS / NVLink
             # transport), read back into the JSON line; to a file, not stdout
@@ -184,7 +194,7 @@ def _barrier(world):
 def _max_over_ranks(v: float, world: int, dev) -> float:
     if world == 1:
         return v
-    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    t = torch.tensor([v], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -344,6 +354,7 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
     a build_db() result of the same database (w.n, xs) to reuse."""
     uq, dev, world, rank, args = c.uq, c.dev, c.world, c.rank, c.args
     d, k, nq = w.d, w.k, w.nq
+    gloo = world > 1 and dist.get_backend() == "gloo"
     if args.shard == "strong":
         from paper_2506_00528_b200.parallel import shard_bounds
         lo, hi = shard_bounds(w.n, world, rank)
@@ -411,10 +422,10 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
             def search_fn(qq, db, dd, kk, id_base=0, **kw):
                 r = uq.search(qq, db, dd, kk, id_base=id_base, **kw)
                 launches[0] += uq.last_launches()
-                return r
+                return (r[0].cpu(), r[1].cpu()) if gloo else r   # gloo exchanges host tensors
 
             def merge_fn(sg, ig, kk, out=None):
-                r = uq.merge_topk(sg, ig, kk, out=out)
+                r = uq.merge_topk(sg.to(dev), ig.to(dev), kk, out=out)
                 launches[0] += uq.last_launches()
                 return r
 
@@ -737,12 +748,14 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the c2 / c5 extra measurements")
     ap.add_argument("--no-f4-index", action="store_true",
                     help="E2M1 pair engine expands the 2-bit codes itself instead of reading the E2M1 index")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test mode for the N>1 code path on one GPU (tests/test_bench_dist.py)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N>1: NCCL allgather + merge, or one merge kernel reading every rank's lists "
                          "from symmetric (peer-mapped) memory")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    world, rank, local = _dist()
+    world, rank, local = _dist(args.dist_backend)
     if args.impl == "reference":
         rc = run_reference(args, world, rank)
         if world > 1:
