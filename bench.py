@@ -274,7 +274,7 @@ def _workload_desc(w, xs):
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
-    w = datagen.CONFIGS[args.config].scaled(n=args.n, nq=args.nq)
+    w = datagen.CONFIGS[args.config].scaled(n=args.db_rows, nq=args.nq)
     xs = _xs(args, w)
     n_s, nq_s, run, cores = _oracle_sample(w, xs, target_s=3.0)
     for _ in range(args.warmup):
@@ -742,8 +742,8 @@ def main():
     ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc", "f4"])
     ap.add_argument("--shard", default="strong", choices=["strong", "weak"],
                     help="strong: the config's N rows split over the G ranks; weak: N rows per rank")
-    ap.add_argument("--n", type=int, default=None, help="override DB rows (global for --shard strong)")
-    ap.add_argument("--nq", type=int, default=None, help="override query batch")
+    ap.add_argument("--db-rows", type=int, default=None, help="override DB rows N (global for --shard strong)")
+    ap.add_argument("--queries", "--nq", dest="nq", type=int, default=None, help="override the query batch Q")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c2 / c5 extra measurements")
     ap.add_argument("--no-f4-index", action="store_true",
@@ -763,7 +763,7 @@ def main():
         return rc
 
     c = Ctx(args, world, rank, local)
-    w = datagen.CONFIGS[args.config].scaled(n=args.n, nq=args.nq)
+    w = datagen.CONFIGS[args.config].scaled(n=args.db_rows, nq=args.nq)
     xs = _xs(args, w)
     r = measure(c, w, xs, args.steps, args.warmup, full=True)
     line = {
@@ -783,7 +783,7 @@ def main():
     line.update(r)
     if world > 1:
         line["comm"] = _nccl_info()
-    if rank == 0 and world == 1 and not args.no_extras and args.config == "c3" and args.n is None:
+    if rank == 0 and world == 1 and not args.no_extras and args.config == "c3" and args.db_rows is None:
         line["extras"] = _extras(c, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, xs)

@@ -394,11 +394,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         const uint32_t sf_tmem = tmem_base + G::SF_COL;
         const uint64_t a_desc0 = smem_desc(smem_u32(sA), A_LBO, SBO);
         const uint64_t b_desc0 = smem_desc(smem_u32(sB), B_LBO, SBO);
+        long long t_loop = PROF_ON ? clk() : 0, t_we = 0, t_wf = 0;
         for (int tile = 0; tile < ntiles; ++tile) {
           const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kAccStride);
           for (int ks = 0; ks < NST; ++ks) {
+            long long t1 = PROF_ON ? clk() : 0;
             if (ks == 0) mbar_wait_cluster(smem_u32(&tempty[acc]), aphase ^ 1u);
+            long long t2 = PROF_ON ? clk() : 0;
+            if (PROF_ON) t_we += t2 - t1;
             mbar_wait_cluster(smem_u32(&full[stage]), sphase);
+            if (PROF_ON) t_wf += clk() - t2;
             tc_fence_after();
             const uint64_t b_stage = b_desc0 + (uint64_t)(((uint32_t)stage * kStageBytes) >> 4);
             if (elect_one()) {
@@ -423,6 +428,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           }
           if (++acc == 2) { acc = 0; aphase ^= 1u; }
         }
+        PROF_ADD(0, clk() - t_loop);
+        PROF_ADD(1, t_we);
+        PROF_ADD(2, t_wf);
+        PROF_ADD(10, 1);
       }
     } else if (warp < kProdWarps) {
       // ================= producers: rows [cr*BH, cr*BH+BH) of each tile =================

@@ -17,7 +17,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ARGS = ["--config", "c2", "--n", "120001", "--nq", "300", "--steps", "3", "--warmup", "3", "--no-extras",
+ARGS = ["--config", "c2", "--db-rows", "120001", "--queries", "300", "--steps", "3", "--warmup", "3", "--no-extras",
         "--no-cpu-baseline"]
 
 

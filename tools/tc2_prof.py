@@ -32,10 +32,13 @@ else:
     ws = torch.empty(uq.search_workspace(w.nq, w.n, w.d, w.k, ALGO), dtype=torch.uint8, device="cuda")
 
 
+IDX = uq.build_f4_index(db, w.d) if (MODE == "f4" and os.environ.get("UQ_PROF_INDEX") == "1") else None
+
+
 def run():
     if MODE == "asym":
         return uq.search_asym(q8, db, w.d, w.k, workspace=ws)
-    return uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws)
+    return uq.search(q, db, w.d, w.k, algo=ALGO, workspace=ws, f4_index=IDX)
 L = uq._L
 L.uq_debug_tc2_prof.argtypes = [ctypes.c_void_p]
 buf = (ctypes.c_ulonglong * 48)()
@@ -49,7 +52,7 @@ for _ in range(reps):
 torch.cuda.synchronize()
 L.uq_debug_tc2_prof(buf)
 c = list(buf)
-out = {"algo": os.environ.get("UQ_PROF_ALGO", "f4"), "cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
+out = {"algo": os.environ.get("UQ_PROF_ALGO", "f4") + ("+index" if IDX is not None else ""), "cfg": cfg, "n": w.n, "nq": w.nq, "k": w.k, "items": c[10],
        "mma_wait_tempty_frac": c[1] / max(c[0], 1), "mma_wait_full_frac": c[2] / max(c[0], 1),
        "prod_wait_empty_frac": c[4] / max(c[3], 1),
        "epi_wait_tfull_frac": c[6] / max(c[5], 1), "epi_filter_frac": c[7] / max(c[5], 1),
