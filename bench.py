@@ -209,7 +209,7 @@ def _oracle_sample(w, xs, target_s: float):
     import oracle
     n_s = min(w.n, 200_000 if w.d <= 768 else 100_000)
     db = datagen.db(w, "cpu", 0, n_s).numpy()
-    q_all = datagen.rows(w, "q", 0, min(w.nq, 1000), "cpu").numpy()
+    q_all = datagen.rows(w, "q", 0, min(w.nq, 4000), "cpu").numpy()
     o_db = {x: oracle.pack(oracle.encode(db, x)) for x in xs}
 
     def run(nq_s):
