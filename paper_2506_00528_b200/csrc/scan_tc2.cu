@@ -65,6 +65,10 @@ constexpr int kOpI8 = 0, kOpF4 = 1;   // operand kind: int8 (kind::i8) / E2M1 (k
 #define UQ_F4_MAX_BPS 8
 #endif
 constexpr int kF4MaxBps = UQ_F4_MAX_BPS;   // f4: at most this many 128-dim blocks per stage
+#ifndef UQ_F4_MAX_BPS_WIDE
+#define UQ_F4_MAX_BPS_WIDE 4
+#endif
+constexpr int kF4MaxBpsWide = UQ_F4_MAX_BPS_WIDE;   // the same for d > 1024
 constexpr int i8_max_bps(int NB) {
   // two stages beside the resident query tile and the seeding histogram (32 KB)
   const int fit = (227 * 1024 - 128 * NB * 128 - 32 * 1024 - 2048) / (2 * 128 * 128);
@@ -89,7 +93,10 @@ template <int OP> struct Geo {
   static constexpr int bps(int NB) {                   // 128-dim blocks per pipeline stage
     // at most mx blocks per stage, split evenly over the fewest stages; int8:
     // mx <= 4 and two stages must fit beside the resident query tile
-    const int mx = OP == kOpI8 ? i8_max_bps(NB) : kF4MaxBps;
+    // f4, d > 1024: the 96 KB query tile leaves room for only two 6-block
+    // stages, i.e. half a tile in flight, and the MMA waited on `full` 54% of
+    // the time on c4 (tools/tc2_prof.py); 4-block stages keep 4 in flight
+    const int mx = OP == kOpI8 ? i8_max_bps(NB) : (NB > 8 ? kF4MaxBpsWide : kF4MaxBps);
     return NB <= mx ? NB : (NB + (NB + mx - 1) / mx - 1) / ((NB + mx - 1) / mx);
   }
   static constexpr int stage_bytes(int NB) { return bps(NB) * BH * RB; }
