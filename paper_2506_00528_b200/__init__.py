@@ -27,6 +27,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # UQ_CHECKED_LIB=1, set before import; everything else loads the product library.
 _LIB_PATH = os.path.join(_HERE, "libuq_prof.so" if os.environ.get("UQ_PROFILE_LIB") == "1" else
                          "libuq_checked.so" if os.environ.get("UQ_CHECKED_LIB") == "1" else "libuq.so")
+# A/B measurements of build variants (tools only): an explicit library path
+_LIB_PATH = os.environ.get("UQ_LIB_AB") or _LIB_PATH
 
 ALGO_AUTO, ALGO_POPC, ALGO_TCGEN05, ALGO_TC_FP4 = 0, 1, 2, 3
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}

@@ -101,6 +101,10 @@ template <int OP> struct Geo {
   }
   static constexpr int stage_bytes(int NB) { return bps(NB) * BH * RB; }
 };
+#ifndef UQ_EPI_PIPE
+#define UQ_EPI_PIPE 1
+#endif
+constexpr bool kEpiPipe = UQ_EPI_PIPE != 0;   // index-fed top-k epilogue: pipelined TMEM loads
 constexpr int kF4Bias = 0x4B400000;   // f32 bits of 1.5 * 2^23: (float)(v) + 1.5*2^23 has bits kF4Bias + v
 // Seeding histogram: 256 bins where shared memory allows (E2M1, d <= 768: a
 // finer bound, fewer main-scan candidates), else 128; two u16 counts per word,
@@ -205,7 +209,10 @@ __device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* 
   }
 }
 
-template <int NB, int MODE, int OP>
+// XM: the stages come from the pre-expanded index by bulk copy (p.dbx set);
+// its instantiation carries no producer expansion code, which keeps the hot
+// loops of the MMA issuer and the epilogue small in the instruction cache.
+template <int NB, int MODE, int OP, bool XM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MODE), 1) scan_tc2_kernel(Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -238,7 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
   uint64_t* tempty = tfull + 2;            // [2] (leader): 2 CTAs x 4 epilogue warps per set
   uint64_t* loaded = tempty + 2;           // [stages] (each CTA): bulk-copy transaction barriers (dbx mode)
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(loaded + p.stages);
-  const bool xmode = p.dbx != nullptr;
+  constexpr bool xmode = XM;
 
   // seed fallback pass with nothing to redo: every thread of both CTAs leaves
   if (p.any_fail != nullptr && *p.any_fail == 0) return;
@@ -441,6 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         PROF_ADD(10, 1);
       }
     } else if (warp < kProdWarps) {
+      if constexpr (!XM) {
       // ================= producers: rows [cr*BH, cr*BH+BH) of each tile =================
       // Warp kMmaWarp of the leader CTA is also the MMA issuer: after writing
       // its rows of a stage it waits for the pair's `full` barrier and issues
@@ -566,6 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         PROF_ADD(2, t_wf);
         PROF_ADD(10, 1);
       }
+      }  // !XM
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4 * kEpiSets) {
       // ================= epilogue =================
       // set h handles accumulator columns [h*BN/2, (h+1)*BN/2) of every tile, so
@@ -724,10 +733,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
           const int thb = OP != kOpF4 ? thrd : raw ? __float_as_int((float)thrd) : max(thrd, -4096) + kF4Bias;
           const uint32_t pad = (OP == kOpF4 && !raw) ? 0u : 0x80000000u;
           const int ncols = (rows - lr0 < CW) ? (int)(rows - lr0) : CW;
-#pragma unroll 1
-          for (int c0 = 0; c0 < ((UQ_DBG(p) & 2) ? 0 : CW); c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(tbase + (uint32_t)c0, v);
+          // one 32-column group of scores (v: columns c0 .. c0 + 31 of this set)
+          auto process = [&](uint32_t (&v)[32], const int c0) {
             if (OP == kOpF4 && !raw) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + 12582912.0f);
@@ -774,10 +781,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                 }
               }
             }
+          };
+          auto release = [&]() {   // this warp is done reading the accumulator
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
+          };
+          if constexpr (XM && kEpiPipe) {
+            // software-pipelined: the TMEM load of group g + 1 is in flight while
+            // group g is filtered, and the accumulator is released as soon as
+            // its last group has been loaded (index-fed kernels only: without
+            // the producer code the two inlined bodies fit the instruction cache)
+            constexpr int NG = (CW + 31) / 32;
+            uint32_t va[32], vb[32];
+            tmem_ld32_nowait(tbase, va);
+#pragma unroll 1
+            for (int g = 0; g < NG; g += 2) {
+              tmem_wait_ld_dep(va);
+              const bool hb = g + 1 < NG;
+              if (hb) tmem_ld32_nowait(tbase + (uint32_t)(32 * (g + 1)), vb);
+              else release();
+              process(va, 32 * g);
+              if (hb) {
+                tmem_wait_ld_dep(vb);
+                if (g + 2 < NG) tmem_ld32_nowait(tbase + (uint32_t)(32 * (g + 2)), va);
+                else release();
+                process(vb, 32 * (g + 1));
+              }
+            }
+          } else {
+#pragma unroll 1
+            for (int c0 = 0; c0 < ((UQ_DBG(p) & 2) ? 0 : CW); c0 += 32) {
+              uint32_t v[32];
+              tmem_ld32(tbase + (uint32_t)c0, v);
+              process(v, c0);
+            }
+            release();
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_dst + (uint32_t)acc * 8u);
           if (++acc == 2) { acc = 0; aphase ^= 1u; }
           long long t2 = PROF_ON ? clk() : 0;
           if (PROF_ON) t_f += t2 - t1;
@@ -1107,7 +1147,7 @@ TcPlan plan_tc2_hist(int64_t nq, int64_t n, int32_t d, int32_t k, int sms, int o
 
 template <int NB, int MODE, int OP>
 static cudaError_t launch_tc2_nb(const tc2::Params& p, const TcPlan& pl, cudaStream_t st) {
-  auto kern = tc2::scan_tc2_kernel<NB, MODE, OP>;
+  auto kern = p.dbx != nullptr ? tc2::scan_tc2_kernel<NB, MODE, OP, true> : tc2::scan_tc2_kernel<NB, MODE, OP, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
   if (e != cudaSuccess) return e;
   kern<<<pl.grid, tc2::Geo<OP>::threads(MODE), pl.smem, st>>>(p);
