@@ -1120,8 +1120,20 @@ static TcPlan plan_tc2_mode(int64_t nq, int64_t n, int32_t d, int32_t k, int sms
     // of codes (the query-tile-major order put each chunk's readers on both
     // dies), for ~1% more scan time (2 of 74 pairs idle)
     if (hi * 20 <= npairs) hi = 0;
-    pl.s_lo = (int32_t)lo;
-    pl.r_hi = (int32_t)hi;
+    // cost of that plan: one round, its largest items (n / lo rows) plus the
+    // fixed per-item cost.  Uniform chunking over several rounds can beat it
+    // when the query tiles are a large fraction of the pairs: c3's seeding
+    // scan (40 tiles, 74 pairs) gave 34 tiles half-size items and left the 6
+    // full-size ones as the critical path
+    double best = (double)((n + lo - 1) / lo) + 8.0 * G::BN;
+    int64_t best_s = -1;
+    for (int64_t sc = lo + 1; sc <= std::min<int64_t>(4 * (lo + 1), s_cap); ++sc) {
+      const double per_item = (double)((n + sc - 1) / sc) + 8.0 * G::BN;
+      const double cost = (double)((QT * sc + npairs - 1) / npairs) * per_item;
+      if (cost < best * 0.97) { best = cost; best_s = sc; }
+    }
+    pl.s_lo = (int32_t)(best_s > 0 ? best_s : lo);
+    pl.r_hi = (int32_t)(best_s > 0 ? 0 : hi);
   }
   const int32_t s_max = pl.s_lo + (pl.r_hi > 0 ? 1 : 0);
   pl.n_chunks = (int64_t)s_max * G::sets(mode);  // lists per query for the merge
