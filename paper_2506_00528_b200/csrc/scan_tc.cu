@@ -246,7 +246,9 @@ __global__ void __launch_bounds__(Cfg<BN>::kThreads, 1) scan_tc_kernel(Params p)
       // ================= epilogue: per-query top-k streams =================
       const int quarter = warp - kEpiWarp0;  // == warp % 4: TMEM lanes 32*quarter..
       int cnt = 0;
-      int thrd = INT32_MIN;  // Delta threshold: a score passes iff Delta > thrd
+      // Delta threshold: a score passes iff Delta > thrd (never for the
+      // padding lanes past the last query)
+      int thrd = q0 + eq < p.nq ? INT32_MIN : INT32_MAX;
       if (p.thr0 && q0 + eq < p.nq) {
         const int32_t dk = p.thr0[(q0 + eq) * p.thr0_stride];
         if (dk != INT32_MIN) thrd = dk - 1;  // pass iff Delta >= D_k

@@ -712,7 +712,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         uint32_t* const my_buf = wbufs + (size_t)lane * p.cap;
         int cnt = 0;
         unsigned n_app = 0, n_reb = 0;   // cycle accounting only: appended keys, in-loop cuts
-        int thrd = INT32_MIN;  // a score passes iff Delta > thrd
+        // a score passes iff Delta > thrd; lanes past the last query (the
+        // zero-padded rows of a partial query tile) never pass -- with
+        // INT32_MIN they appended every score of every tile (c3's last tile
+        // holds 16 queries and 240 padding lanes) and cut their buffers
+        // constantly, stretching those items
+        int thrd = qme < p.nq ? INT32_MIN : (1 << 24);   // 2^24 > |score| (<= 127 d)
         if (p.thr0 && qme < p.nq) {
           const int32_t dk = p.thr0[qme * p.thr0_stride];
           if (dk != INT32_MIN) thrd = dk - 1;
