@@ -860,8 +860,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
         // publish: 8 streams x 4 entries per lane per round, all loads issued
         // before the stores (a stream-at-a-time loop serialised ~100 L2 round
         // trips per warp: 25 us of every work item's tail on c2)
+        {
+          const int64_t qi = q0 + quarter * 32 + lane;   // this lane's stream: its list's count
+          if (qi < p.nq) p.part_cnt[(size_t)(it.c * kEpiSets + h) * p.nq + qi] = cnt;   // entries past it are never read
+        }
+        const int cmax = (int)__reduce_max_sync(kFull, (unsigned)cnt);   // rounds past it would move nothing
         for (int L0 = 0; L0 < 32; L0 += 8) {
-          for (int i0 = 0; i0 < p.cap; i0 += 128) {
+          for (int i0 = 0; i0 < cmax; i0 += 128) {
             uint32_t t[8][4];
             int cLs[8];
 #pragma unroll
@@ -882,7 +887,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
               uint64_t* out = p.part + list * p.cap;
               const int cv = cLs[u];
               UQ_ASSERT(cv <= p.cap && it.c < p.s_max);
-              if (i0 == 0 && lane == 0) p.part_cnt[list] = cv;   // entries past it are never read
 #pragma unroll
               for (int v = 0; v < 4; ++v) {
                 const int i = i0 + 32 * v + lane;
