@@ -372,10 +372,18 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
     u_q = datagen.queries(w, dev)
     u_q_host = u_q.cpu().pin_memory()
 
-    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4}[args.algo]
+    # --algo asym: single-operand search -- int8-quantised float
+    # queries (uq_quantize_i8, R15) x the ternary DB by masked addition
+    # (uq_search_asym) on the int8 pair engine, fed by the int8 index
+    asym = args.algo == "asym"
+    algo = {"auto": uq.ALGO_AUTO, "popc": uq.ALGO_POPC, "tc": uq.ALGO_TCGEN05, "f4": uq.ALGO_TC_FP4,
+            "asym": uq.ALGO_TCGEN05}[args.algo]
     resolved = uq.search_resolve(nq, n_loc, d, k, algo)
-    use_x = (not args.no_f4_index) and resolved == uq.ALGO_TC_FP4
-    f4x, idx_ms = {}, None
+    use_x = (not args.no_f4_index) and resolved == uq.ALGO_TC_FP4 and not asym
+    f4x, i8x, idx_ms = {}, {}, None
+    if asym and not args.no_f4_index and d <= 1024:
+        for x in xs:
+            i8x[x] = uq.build_i8_index(codes[x], d)
     if use_x:
         for x in xs:
             f4x[x] = uq.build_f4_index(codes[x], d)
@@ -395,8 +403,10 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
         torch.cuda.synchronize()
         enc_whole_ms = e0.elapsed_time(e1)
 
-    ws = torch.empty(max(uq.search_workspace(nq, n_loc, d, k, uq.ALGO_TC_FP4 if use_x else algo), 1),
+    ws = torch.empty(max(uq.search_asym_workspace(nq, n_loc, d, k) if asym else
+                         uq.search_workspace(nq, n_loc, d, k, uq.ALGO_TC_FP4 if use_x else algo), 1),
                      dtype=torch.uint8, device=dev)
+    q8 = torch.empty((nq, d), dtype=torch.int8, device=dev) if asym else None
     qc = torch.empty((nq, uq.code_bytes(d)), dtype=torch.uint8, device=dev)
     loc = (torch.empty((nq, k), dtype=torch.int32, device=dev), torch.empty((nq, k), dtype=torch.int64, device=dev))
     launches = [0]
@@ -416,11 +426,19 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
         for j, x in enumerate(xs):
             if marks is not None:
                 marks[j].record()
-            uq.encode(q_dev, x, out=qc)
+            if asym:
+                uq.quantize_i8(q_dev, out=q8)
+            else:
+                uq.encode(q_dev, x, out=qc)
             launches[0] += uq.last_launches()
 
             def search_fn(qq, db, dd, kk, id_base=0, **kw):
-                r = uq.search(qq, db, dd, kk, id_base=id_base, **kw)
+                if asym:
+                    kw.pop("algo", None)
+                    kw.pop("f4_index", None)
+                    r = uq.search_asym(q8, db, dd, kk, id_base=id_base, i8_index=i8x.get(x), **kw)
+                else:
+                    r = uq.search(qq, db, dd, kk, id_base=id_base, **kw)
                 launches[0] += uq.last_launches()
                 return (r[0].cpu(), r[1].cpu()) if gloo else r   # gloo exchanges host tensors
 
@@ -540,7 +558,7 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
     value = evals_step * steps / (ms * 1e-3)
     peaks, peaks_src = _peaks()
     roof = _roofline(c, w, nq, n_loc, d, algo, use_x, main_ms, main_n, main_evals, seed_ms, seed_n, seed_evals,
-                     ms, peaks, peaks_src)
+                     ms, peaks, peaks_src, asym=asym, i8x=bool(i8x))
     res = {
         "value": value, "ms_per_step": ms / steps, "qps": len(xs) * nq * steps / (ms * 1e-3),
         "per_gpu": {"delta_evals_per_s": value / world, "qps": len(xs) * nq * steps / (ms * 1e-3) / world,
@@ -553,6 +571,7 @@ def measure(c: Ctx, w, xs, steps: int, warmup: int, full: bool = True, prebuilt=
         "db_rows_global": n_global, "db_rows_per_gpu": n_loc, "shard": args.shard,
         "index": {"codes_bytes": n_loc * uq.code_bytes(d) * len(xs),
                   "f4_index_bytes": sum(int(t.numel()) for t in f4x.values()),
+                  "i8_index_bytes": sum(int(t.numel()) for t in i8x.values()),
                   "f4_index_build_ms": idx_ms,
                   "note": ("E2M1 operand image of the codes (4 bits per dim), one per x, built once with the "
                            "index" if f4x else "2-bit codes only")},
@@ -589,14 +608,15 @@ def _encode_stats(uq, w, xs, n_loc, enc_ms, enc_whole_ms, peaks, t_gen):
 
 
 def _roofline(c, w, nq, n_loc, d, algo, use_x, main_ms, main_n, main_evals, seed_ms, seed_n, seed_evals, ms,
-              peaks, peaks_src):
+              peaks, peaks_src, asym=False, i8x=False):
     uq = c.uq
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(c.dev).multi_processor_count
     resolved = uq.search_resolve(nq, n_loc, d, w.k, algo)
-    used_f4 = resolved == uq.ALGO_TC_FP4
-    used_tc = resolved in (uq.ALGO_TCGEN05, uq.ALGO_TC_FP4)
-    algo_name = "tcgen05-f4-index" if use_x else "tcgen05-f4" if used_f4 else "tcgen05" if used_tc else "popc"
+    used_f4 = resolved == uq.ALGO_TC_FP4 and not asym
+    used_tc = resolved in (uq.ALGO_TCGEN05, uq.ALGO_TC_FP4) or asym
+    algo_name = ("tcgen05-asym-int8" + ("-index" if i8x else "")) if asym else \
+        "tcgen05-f4-index" if use_x else "tcgen05-f4" if used_f4 else "tcgen05" if used_tc else "popc"
     scan_avg_s = (main_ms / max(main_n, 1)) * 1e-3
     evals_per_launch = main_evals / max(main_n, 1)
     if used_f4:
@@ -618,7 +638,9 @@ def _roofline(c, w, nq, n_loc, d, algo, use_x, main_ms, main_n, main_evals, seed
         achieved = ops / scan_avg_s / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": ("scan_tc2_kernel (CTA-pair int8 tcgen05 Delta GEMM + fused top-k)"
+                "kernel": ("scan_tc2_kernel<NB,0,0> (CTA-pair int8 tcgen05, int8 queries as the A operand: "
+                           "masked-addition scores + fused top-k)" if asym else
+                           "scan_tc2_kernel (CTA-pair int8 tcgen05 Delta GEMM + fused top-k)"
                            if nq > 128 and d <= 1024 else "scan_tc_kernel (int8 tcgen05 Delta GEMM + fused top-k)"),
                 "peak_source": f"2 x bf16_tflops of {peaks_src} MEASURED_PEAKS.json (int8 = 2x bf16 nominal)",
                 "algorithmic": "2*d ops per Delta (d int8 MACs)", "_dtype": "s8"}
@@ -739,7 +761,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(datagen.CONFIGS))
     ap.add_argument("--x", default=None, help="comma-separated x values (default: the config's sweep)")
-    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc", "f4"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "popc", "tc", "f4", "asym"],
+                    help="asym: single-operand search (P:507-509), int8 queries x ternary DB")
     ap.add_argument("--shard", default="strong", choices=["strong", "weak"],
                     help="strong: the config's N rows split over the G ranks; weak: N rows per rank")
     ap.add_argument("--db-rows", type=int, default=None, help="override DB rows N (global for --shard strong)")
