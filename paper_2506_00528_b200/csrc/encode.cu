@@ -40,6 +40,7 @@
 #include "common.cuh"
 #include "internal.h"
 
+
 namespace uq {
 
 template <typename T> struct ElemBits;
@@ -527,6 +528,226 @@ encode_kernel(const T* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp16 rows: a leaner kernel for the same search (c5's DB encode).  The generic
+// kernel spent ~716 warp instructions per d=768 row, ALU-pipe bound (ncu:
+// issue 76%, ALU 72%; profiles/r02/enc_f16_*).  Here:
+//  * the raw words keep their signs; |u| comes from the HSET2 operand modifier
+//    (no sign-clearing pass, no separate sign mask);
+//  * a count pass is 2 instructions per two keys (HSET2.BF + HADD2) plus 3 for
+//    the warp total: the per-half sums start at 512 so lo + hi = 1024 + n is an
+//    f16 whose low bits are n (HADD2 + LOP3 + REDUX, no float conversions);
+//  * the interpolation runs in key space (integer keys are piecewise linear in
+//    |u|) and the forced bisections start only after 4 interpolated passes;
+//    T*/RMS is tracked as an average over the warp's rows (measured in a
+//    simulator of this search on c5 rows: 4.08 -> 3.42 passes per row);
+//  * selected bits come straight from signed compares (u >= T: +1, u <= -T:
+//    -1), assembled by LOP3 from the HSET2 masks, and each lane stores its
+//    plane bytes directly (one 32-byte sector per warp store).
+// Exactness is as in the generic kernel: every decision is an exact compare
+// of f16 magnitudes (HSET2 is exact on f16, subnormals included).
+__device__ __forceinline__ __half2 h2(uint32_t w) { return *reinterpret_cast<const __half2*>(&w); }
+
+// Warp total of count(|u| >= c) over this lane's NW half pairs, BIASED by
+// kF16Bias: each lane's half sums start at 512, so lo + hi = 1024 + n is an f16
+// whose bit pattern is 0x6400 + n (n <= 2*NW < 1024: exact).  The search
+// compares biased counts with x + kF16Bias and never unbiases them.
+constexpr uint32_t kF16Bias = 32u * 0x6400u;
+template <int NW>
+__device__ __forceinline__ unsigned f16_count_ge(const uint32_t (&w)[NW], uint32_t c2) {  // c2 = c | c << 16
+  const __half2 cc = h2(c2);
+  __half2 acc = h2(0x60006000u);  // (512, 512)
+#pragma unroll
+  for (int i = 0; i < NW; ++i) acc = __hadd2(acc, __hge2(__habs2(h2(w[i])), cc));
+  const __half s = __hadd(__low2half(acc), __high2half(acc));
+  return __reduce_add_sync(kFull, (unsigned)__half_as_ushort(s));
+}
+__device__ __forceinline__ uint32_t dup16(uint32_t c) { return __byte_perm(c, 0u, 0x1010); }
+
+// 8 flags (bit 2k + h = half h of m_k, from HSET2 masks 0xffff/0) -> low byte
+__device__ __forceinline__ uint32_t mask8(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+  uint32_t t = m0 & 0x00020001u;
+  t |= m1 & 0x00080004u;
+  t |= m2 & 0x00200010u;
+  t |= m3 & 0x00800040u;
+  return t | (t >> 16);   // bits 0..7 (upper bits: don't care, stored as a byte)
+}
+
+// 8 flags as HSET2.BF halves (1.0 / 0.0; b_k = elements 2k, 2k+1) -> 0x6400 + byte
+// in the low 16 bits: weighted sums on the FP16 pipe (HFMA2), exact small
+// integers, the 1024.0 bias puts the byte in the low 8 bits of the f16 pattern
+__device__ __forceinline__ uint32_t bits8_bf(__half2 b0, __half2 b1, __half2 b2, __half2 b3) {
+  __half2 acc = h2(0x00006400u);                     // (1024, 0)
+  acc = __hfma2(b0, h2(0x40003c00u), acc);           // (1, 2)
+  acc = __hfma2(b1, h2(0x48004400u), acc);           // (4, 8)
+  acc = __hfma2(b2, h2(0x50004c00u), acc);           // (16, 32)
+  acc = __hfma2(b3, h2(0x58005400u), acc);           // (64, 128)
+  return (uint32_t)__half_as_ushort(__hadd(__low2half(acc), __high2half(acc)));
+}
+
+__device__ __forceinline__ float rsqrt_approx(float v) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// FULL: 16-byte aligned rows with d == 256 * NCH (every chunk a full vector
+// load, plane bytes = 32 * NCH): no per-chunk bounds.
+template <int NCH, bool VECLOAD, bool FULL>
+__global__ void __launch_bounds__(kEncWarps * 32, NCH <= 4 ? 4 : 3)
+encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t x, float z0, float delta,
+                  uint8_t* __restrict__ codes) {
+  constexpr int NW = 4 * NCH;                 // half pairs per lane
+  constexpr int NS = NCH < 2 ? NCH : 2;       // chunks sampled for the RMS
+  constexpr uint32_t kEnd = 0x7c01u;          // finite keys are < kEnd (inf / NaN: precondition, R4)
+  const int lane = threadIdx.x & 31;
+  const int64_t pb = FULL ? 32 * NCH : plane_bytes(d);
+  const int64_t cb = 2 * pb;
+  const int64_t warp_global = (int64_t)blockIdx.x * kEncWarps + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kEncWarps;
+  const float inv_ns = 1.0f / (float)min(d, 256 * NS);
+  const unsigned xb = (unsigned)x + kF16Bias;
+  const int64_t ustep = nwarps * ld, cstep = nwarps * cb;
+  float ratio = z0;   // T* / RMS, averaged over this warp's rows
+  auto load_row = [&](const __half* src, uint4 (&r)[NCH]) {
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      if constexpr (FULL) r[j] = __ldg(reinterpret_cast<const uint4*>(src + j * 256 + lane * 8));
+      else r[j] = load_chunk<__half, VECLOAD>(src, j * 256 + lane * 8, d);
+    }
+  };
+  // L2 prefetch of the row two iterations ahead: one 128-byte line per lane
+  const bool pf_lane = VECLOAD && lane * 64 < d;
+
+  uint4 raw[NCH];
+  const __half* up = u + warp_global * ld;
+  uint8_t* cp = codes + warp_global * cb;
+  if (warp_global < n) load_row(up, raw);
+  for (int64_t row = warp_global; row < n; row += nwarps, up += ustep, cp += cstep) {
+    if (pf_lane && row + 2 * nwarps < n)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(up + 2 * ustep + lane * 64) : "memory");
+    uint32_t w[NW];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      w[4 * j] = raw[j].x; w[4 * j + 1] = raw[j].y; w[4 * j + 2] = raw[j].z; w[4 * j + 3] = raw[j].w;
+    }
+    // ---- scale estimate: mean |u| (HFMA2 of |u| * 2^-6; steering only) ----
+    float ss;
+    {
+      __half2 acc = __float2half2_rn(0.f);
+      const __half2 sc = __float2half2_rn(0.015625f);
+#pragma unroll
+      for (int i = 0; i < 4 * NS; ++i) acc = __hfma2(__habs2(h2(w[i])), sc, acc);
+      ss = (__low2float(acc) + __high2float(acc)) * 64.f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+    const float rms = ss * inv_ns;
+
+    // ---- T* = x-th largest key: count(>= lo) >= x > count(>= hi) (counts biased) ----
+    uint32_t lo = 0u, hi = kEnd, Tk = 0u;
+    unsigned clo = 256u * NCH + kF16Bias, chi = kF16Bias;
+    bool exact = false;
+    {
+      const float t = rms * ratio;
+      // both probes in one packed conversion; clamped to [1, 0x7bff] per half
+      const uint32_t pp = __vminu2(__vmaxu2(h2_bits(__floats2half2_rn(t * (1.f - delta), t * (1.f + delta))) & 0x7fff7fffu,
+                                            0x00010001u), 0x7bff7bffu);
+      const uint32_t p1 = pp & 0xffffu;
+      const uint32_t p2 = max(pp >> 16, p1 + 1u);
+      const unsigned n1 = f16_count_ge<NW>(w, dup16(p1));
+      const unsigned n2 = f16_count_ge<NW>(w, dup16(p2));
+      // n1 >= n2 (p1 < p2)
+      if (n1 == xb) { Tk = p1; exact = true; }
+      else if (n2 == xb) { Tk = p2; exact = true; }
+      else if (n2 > xb) { lo = p2; clo = n2; }
+      else if (n1 > xb) { lo = p1; clo = n1; hi = p2; chi = n2; }
+      else { hi = p1; chi = n1; }
+    }
+    unsigned sec = 4u;   // interpolated passes before the forced bisections start
+#pragma unroll 1
+    while (!exact && hi - lo > 1u) {
+      uint32_t c;
+      if (hi == kEnd || sec == 0u) {
+        c = lo + ((hi - lo) >> 1);                 // guaranteed progress
+        sec = 1u;
+      } else {
+        const float f = ((float)(clo - xb) + 0.5f) * rcp_approx((float)(clo - chi));
+        c = lo + (uint32_t)(f * (float)(hi - lo));
+        c = min(max(c, lo + 1u), hi - 1u);
+        --sec;
+      }
+      const unsigned cnt = f16_count_ge<NW>(w, dup16(c));
+      exact = cnt == xb;
+      const bool up_ = cnt > xb;
+      Tk = c;
+      lo = up_ ? c : lo;
+      clo = up_ ? cnt : clo;
+      hi = up_ ? hi : c;
+      chi = up_ ? chi : cnt;
+    }
+    if (!exact) { Tk = lo; exact = (clo == xb); }
+    if (Tk != 0u && rms > 0.f) {
+      const float rn = __fdividef(ElemBits<__half>::key2f(Tk), rms);
+      if (rn > 0.f && rn < 1e30f) ratio = fmaf(0.3f, rn - ratio, ratio);
+    }
+
+    // ---- plane bytes: +1 where u >= T, -1 where u <= -T (T >= 1: zeros never) ----
+    uint32_t posb[NCH], negb[NCH];
+    if (exact || Tk == 0u) {
+      // exact: the keys >= Tk are the x largest.  Tk == 0: fewer than x
+      // non-zero magnitudes -> every non-zero is selected (R2).
+      const uint32_t ts = (Tk == 0u) ? 1u : Tk;
+      const __half2 tp = h2(dup16(ts)), tn = h2(dup16(ts | 0x8000u));
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        posb[j] = bits8_bf(__hge2(h2(w[4 * j]), tp), __hge2(h2(w[4 * j + 1]), tp),
+                           __hge2(h2(w[4 * j + 2]), tp), __hge2(h2(w[4 * j + 3]), tp));
+        negb[j] = bits8_bf(__hle2(h2(w[4 * j]), tn), __hle2(h2(w[4 * j + 1]), tn),
+                           __hle2(h2(w[4 * j + 2]), tn), __hle2(h2(w[4 * j + 3]), tn));
+      }
+    } else {
+      // ties at T* (count(>= T) = clo > x > chi = count(> T)): keys > T plus
+      // the first x - chi keys == T in index order (chunk, lane, element; R1)
+      const __half2 tp = h2(dup16(Tk)), tn = h2(dup16(Tk | 0x8000u));
+      int need = (int)(xb - chi);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const uint32_t gp = mask8(__hgt2_mask(h2(w[4 * j]), tp), __hgt2_mask(h2(w[4 * j + 1]), tp),
+                                  __hgt2_mask(h2(w[4 * j + 2]), tp), __hgt2_mask(h2(w[4 * j + 3]), tp)) & 0xffu;
+        const uint32_t gn = mask8(__hlt2_mask(h2(w[4 * j]), tn), __hlt2_mask(h2(w[4 * j + 1]), tn),
+                                  __hlt2_mask(h2(w[4 * j + 2]), tn), __hlt2_mask(h2(w[4 * j + 3]), tn)) & 0xffu;
+        const uint32_t ep = mask8(__heq2_mask(h2(w[4 * j]), tp), __heq2_mask(h2(w[4 * j + 1]), tp),
+                                  __heq2_mask(h2(w[4 * j + 2]), tp), __heq2_mask(h2(w[4 * j + 3]), tp)) & 0xffu;
+        const uint32_t en = mask8(__heq2_mask(h2(w[4 * j]), tn), __heq2_mask(h2(w[4 * j + 1]), tn),
+                                  __heq2_mask(h2(w[4 * j + 2]), tn), __heq2_mask(h2(w[4 * j + 3]), tn)) & 0xffu;
+        uint32_t eq = ep | en;
+        const int ce = __popc(eq);
+        int incl = ce;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int tv = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += tv;
+        }
+        const int take = min(max(need - (incl - ce), 0), ce);   // keep the lowest `take` bits of eq
+        while (__popc(eq) > take) eq &= ~(0x80000000u >> __clz(eq));
+        need -= __shfl_sync(kFull, incl, 31);
+        posb[j] = gp | (eq & ep);
+        negb[j] = gn | (eq & en);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int64_t bi = 32 * j + lane;
+      if (FULL || bi < pb) {
+        cp[bi] = (uint8_t)posb[j];
+        cp[pb + bi] = (uint8_t)negb[j];
+      }
+    }
+    if (row + nwarps < n) load_row(up + ustep, raw);
+  }
+}
+
 // Phi^-1(p) for p in (0, 1) (Acklam's rational approximation; only steers the
 // probes of the search, never decides a bit)
 float inv_norm_cdf(double p) {
@@ -577,7 +798,21 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
     const char* e = getenv("UQ_ENC_DELTA");
     return e ? (float)atof(e) : 0.f;
   }();
-  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.12f : 0.08f);
+  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.12f : std::is_same<T, __half>::value ? 0.05f : 0.08f);
+  if constexpr (std::is_same<T, __half>::value) {
+    z0 *= 1.2533141f;   // the f16 kernel steers by mean |u| = s * sqrt(2 / pi) for N(0, s^2)
+    if (vec && d == 256 * NCH)
+      encode_f16_kernel<NCH, true, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
+          (const __half*)u, n, d, ld, x, z0, delta, codes);
+    else if (vec)
+      encode_f16_kernel<NCH, true, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
+          (const __half*)u, n, d, ld, x, z0, delta, codes);
+    else
+      encode_f16_kernel<NCH, false, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
+          (const __half*)u, n, d, ld, x, z0, delta, codes);
+    note_launch();
+    return cudaGetLastError();
+  }
   if (vec)
     encode_kernel<T, NCH, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
         (const T*)u, n, d, ld, x, z0, delta, codes);
