@@ -648,6 +648,7 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
     uint32_t lo = 0u, hi = kEnd, Tk = 0u;
     unsigned clo = 256u * NCH + kF16Bias, chi = kF16Bias;
     bool exact = false;
+    float islope;
     {
       const float t = rms * ratio;
       // both probes in one packed conversion; clamped to [1, 0x7bff] per half
@@ -657,6 +658,9 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
       const uint32_t p2 = max(pp >> 16, p1 + 1u);
       const unsigned n1 = f16_count_ge<NW>(w, dup16(p1));
       const unsigned n2 = f16_count_ge<NW>(w, dup16(p2));
+      // keys per unit of count between the probes (extrapolation when T* is
+      // outside them)
+      islope = (float)(p2 - p1) * rcp_approx((float)max(n1 - n2, 1u));
       // n1 >= n2 (p1 < p2)
       if (n1 == xb) { Tk = p1; exact = true; }
       else if (n2 == xb) { Tk = p2; exact = true; }
@@ -664,11 +668,18 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
       else if (n1 > xb) { lo = p1; clo = n1; hi = p2; chi = n2; }
       else { hi = p1; chi = n1; }
     }
-    unsigned sec = 4u;   // interpolated passes before the forced bisections start
+    unsigned sec = 6u;   // interpolated passes before the forced bisections start
 #pragma unroll 1
     while (!exact && hi - lo > 1u) {
       uint32_t c;
-      if (hi == kEnd || sec == 0u) {
+      if (hi == kEnd || lo == 0u) {
+        // T* outside the probes: step past the nearer one by the probes'
+        // slope (doubling each time the step falls short)
+        const uint32_t s = (uint32_t)(((float)(hi == kEnd ? clo - xb : xb - chi) + 0.5f) * islope) + 1u;
+        c = hi == kEnd ? lo + s : (hi > s ? hi - s : 0u);
+        c = min(max(c, lo + 1u), hi - 1u);
+        islope *= 2.f;
+      } else if (sec == 0u) {
         c = lo + ((hi - lo) >> 1);                 // guaranteed progress
         sec = 1u;
       } else {
@@ -798,7 +809,7 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
     const char* e = getenv("UQ_ENC_DELTA");
     return e ? (float)atof(e) : 0.f;
   }();
-  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.12f : std::is_same<T, __half>::value ? 0.05f : 0.08f);
+  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.12f : std::is_same<T, __half>::value ? 0.03f : 0.08f);
   if constexpr (std::is_same<T, __half>::value) {
     z0 *= 1.2533141f;   // the f16 kernel steers by mean |u| = s * sqrt(2 / pi) for N(0, s^2)
     if (vec && d == 256 * NCH)
