@@ -553,12 +553,12 @@ __device__ __forceinline__ __half2 h2(uint32_t w) { return *reinterpret_cast<con
 // whose bit pattern is 0x6400 + n (n <= 2*NW < 1024: exact).  The search
 // compares biased counts with x + kF16Bias and never unbiases them.
 constexpr uint32_t kF16Bias = 32u * 0x6400u;
-template <int NW>
+template <int NW, bool ABS = true>
 __device__ __forceinline__ unsigned f16_count_ge(const uint32_t (&w)[NW], uint32_t c2) {  // c2 = c | c << 16
   const __half2 cc = h2(c2);
   __half2 acc = h2(0x60006000u);  // (512, 512)
 #pragma unroll
-  for (int i = 0; i < NW; ++i) acc = __hadd2(acc, __hge2(__habs2(h2(w[i])), cc));
+  for (int i = 0; i < NW; ++i) acc = __hadd2(acc, __hge2(ABS ? __habs2(h2(w[i])) : h2(w[i]), cc));
   const __half s = __hadd(__low2half(acc), __high2half(acc));
   return __reduce_add_sync(kFull, (unsigned)__half_as_ushort(s));
 }
@@ -759,6 +759,229 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
   }
 }
 
+// ---------------------------------------------------------------------------
+// f32 rows (c2-c4 DB encodes): the f16 kernel's structure on the f32 search.
+// The generic kernel spent ~850 warp instructions per d=768 row (ncu: ALU pipe
+// 78%, issue 77%; profiles/r02/enc_f32_*).  Here:
+//  * raw words keep their signs; the coarse keys (top 16 bits of |u|, compared
+//    as f16 patterns, clamped below the f16 inf pattern) come from one PRMT +
+//    HMNMX2(|.|) per two elements;
+//  * the coarse search is the f16 kernel's (biased HSET2/HADD2 counts,
+//    key-space interpolation, slope extrapolation when T* is outside the
+//    probes); coarse(a) > coarse(b) => key(a) > key(b), so it brackets T*
+//    exactly, and only a one-coarse-value bracket (a few elements) goes to
+//    full 32-bit counts (abs keys built once, on demand);
+//  * selection by signed integer compares of the raw bits (u >= T as int32:
+//    +1; u >= T | 2^31 as uint32: -1), one nibble per plane per chunk;
+//  * lane pairs swap nibbles with one shuffle per chunk; even lanes store the
+//    + plane byte, odd lanes the - plane byte (one store per chunk per warp).
+template <int NCH, bool VECLOAD, bool FULL>
+__global__ void __launch_bounds__(kEncWarps * 32, NCH > 8 ? 2 : 3)
+encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t x, float z0, float delta,
+                  uint8_t* __restrict__ codes) {
+  constexpr int E = 4 * NCH;                  // elements per lane
+  constexpr int NWC = 2 * NCH;                // coarse half pairs per lane
+  constexpr int NS = NCH < 2 ? NCH : NCH / 2; // chunks sampled for the RMS
+  constexpr uint32_t kCEnd = 0x7c00u;         // coarse keys are <= 0x7bff
+  const int lane = threadIdx.x & 31;
+  const int64_t pb = FULL ? 16 * NCH : plane_bytes(d);
+  const int64_t cb = 2 * pb;
+  const int64_t warp_global = (int64_t)blockIdx.x * kEncWarps + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kEncWarps;
+  const float inv_ns = 1.0f / (float)min(d, 128 * NS);
+  const unsigned xb = (unsigned)x + kF16Bias;
+  const int64_t ustep = nwarps * ld, cstep = nwarps * cb;
+  float ratio = z0;   // T* / RMS, averaged over this warp's rows
+  auto load_row = [&](const float* src, uint4 (&r)[NCH]) {
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      if constexpr (FULL) r[j] = __ldg(reinterpret_cast<const uint4*>(src + j * 128 + lane * 4));
+      else r[j] = load_chunk<float, VECLOAD>(src, j * 128 + lane * 4, d);
+    }
+  };
+  const bool pf_lane = VECLOAD && lane * 32 < d;   // one 128-byte line per lane
+
+  uint4 raw[NCH];
+  const float* up = u + warp_global * ld;
+  uint8_t* cp = codes + warp_global * cb;
+  if (warp_global < n) load_row(up, raw);
+  for (int64_t row = warp_global; row < n; row += nwarps, up += ustep, cp += cstep) {
+    if (pf_lane && row + 2 * nwarps < n)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(up + 2 * ustep + lane * 32) : "memory");
+    uint32_t r[E];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      r[4 * j] = raw[j].x; r[4 * j + 1] = raw[j].y; r[4 * j + 2] = raw[j].z; r[4 * j + 3] = raw[j].w;
+    }
+    // ---- RMS estimate (FFMA; steering only) ----
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4 * NS; ++i) ss = fmaf(__uint_as_float(r[i]), __uint_as_float(r[i]), ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(kFull, ss, o);
+    ss *= inv_ns;
+    const float rms = (ss > 0.f) ? ss * rsqrt_approx(ss) : 0.f;
+
+    // ---- coarse keys: min(top 16 bits of |u|, 0x7bff) as f16 patterns ----
+    uint32_t cw[NWC];
+#pragma unroll
+    for (int i = 0; i < NWC; ++i)
+      cw[i] = h2_bits(__hmin2(__habs2(h2(__byte_perm(r[2 * i], r[2 * i + 1], 0x7632))), h2(0x7bff7bffu)));
+
+    // ---- coarse search: count(>= lo) >= x > count(>= hi) (biased counts) ----
+    uint32_t lo = 0u, hi = kCEnd, Tk = 0u;
+    unsigned clo = 128u * NCH + kF16Bias, chi = kF16Bias;
+    bool exact = false;
+    float islope;
+    {
+      const float t = rms * ratio;
+      const uint32_t q1 = __float_as_uint(t * (1.f - delta)) >> 16, q2 = __float_as_uint(t * (1.f + delta)) >> 16;
+      const uint32_t p1 = min(max(q1 & 0x7fffu, 1u), 0x7bfeu);
+      const uint32_t p2 = min(max(q2 & 0x7fffu, p1 + 1u), 0x7bffu);
+      const unsigned n1 = f16_count_ge<NWC, false>(cw, dup16(p1));
+      const unsigned n2 = f16_count_ge<NWC, false>(cw, dup16(p2));
+      islope = (float)(p2 - p1) * rcp_approx((float)max(n1 - n2, 1u));
+      if (n1 == xb) { Tk = p1; exact = true; }
+      else if (n2 == xb) { Tk = p2; exact = true; }
+      else if (n2 > xb) { lo = p2; clo = n2; }
+      else if (n1 > xb) { lo = p1; clo = n1; hi = p2; chi = n2; }
+      else { hi = p1; chi = n1; }
+    }
+    {
+      unsigned sec = 6u;
+#pragma unroll 1
+      while (!exact && hi - lo > 1u) {
+        uint32_t c;
+        if (hi == kCEnd || lo == 0u) {
+          const uint32_t s = (uint32_t)(((float)(hi == kCEnd ? clo - xb : xb - chi) + 0.5f) * islope) + 1u;
+          c = hi == kCEnd ? lo + s : (hi > s ? hi - s : 0u);
+          c = min(max(c, lo + 1u), hi - 1u);
+          islope *= 2.f;
+        } else if (sec == 0u) {
+          c = lo + ((hi - lo) >> 1);
+          sec = 1u;
+        } else {
+          const float f = ((float)(clo - xb) + 0.5f) * rcp_approx((float)(clo - chi));
+          c = lo + (uint32_t)(f * (float)(hi - lo));
+          c = min(max(c, lo + 1u), hi - 1u);
+          --sec;
+        }
+        const unsigned cnt = f16_count_ge<NWC, false>(cw, dup16(c));
+        exact = cnt == xb;
+        const bool up_ = cnt > xb;
+        Tk = c;
+        lo = up_ ? c : lo;
+        clo = up_ ? cnt : clo;
+        hi = up_ ? hi : c;
+        chi = up_ ? chi : cnt;
+      }
+    }
+    if (exact) {
+      Tk <<= 16;                      // keys >= Tc << 16 <=> coarse >= Tc: exactly x of them
+    } else {
+      // ---- full keys inside one coarse value: [lc << 16, hc << 16) ----
+      const unsigned xu = (unsigned)x;
+      uint32_t flo = lo << 16, fhi = (hi == kCEnd) ? 0x80000000u : (hi << 16);
+      unsigned fclo = clo - kF16Bias, fchi = (hi == kCEnd) ? 0u : chi - kF16Bias;
+      uint32_t kk[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) kk[e] = r[e] & 0x7fffffffu;
+      unsigned sec = 3u;
+#pragma unroll 1
+      while (!exact && fhi - flo > 1u) {
+        uint32_t c;
+        if (sec == 0u || fhi == 0x80000000u) {
+          c = flo + ((fhi - flo) >> 1);
+          sec = 1u;
+        } else {
+          const float f = ((float)(fclo - xu) + 0.5f) * rcp_approx((float)(fclo - fchi));
+          c = flo + (uint32_t)(f * (float)(fhi - flo));
+          c = min(max(c, flo + 1u), fhi - 1u);
+          --sec;
+        }
+        unsigned a0 = 0u, a1 = 0u;
+#pragma unroll
+        for (int e = 0; e < E; e += 2) {
+          a0 = add_lt(a0, kk[e], c);
+          a1 = add_lt(a1, kk[e + 1], c);
+        }
+        const unsigned cnt = __reduce_add_sync(kFull, (unsigned)E - a0 - a1);
+        exact = cnt == xu;
+        const bool up_ = cnt > xu;
+        Tk = c;
+        flo = up_ ? c : flo;
+        fclo = up_ ? cnt : fclo;
+        fhi = up_ ? fhi : c;
+        fchi = up_ ? fchi : cnt;
+      }
+      if (!exact) { Tk = flo; exact = (fclo == xu); chi = fchi; }
+    }
+    if (Tk != 0u && rms > 0.f) {
+      const float rn = __fdividef(__uint_as_float(Tk), rms);
+      if (rn > 0.f && rn < 1e30f) ratio = fmaf(0.3f, rn - ratio, ratio);
+    }
+
+    // ---- nibbles (bits 0-3: +1 where u >= T; bits 4-7: -1 where u <= -T) ----
+    uint32_t nib[NCH];
+    if (exact || Tk == 0u) {
+      const int32_t ti = (int32_t)((Tk == 0u) ? 1u : Tk);
+      const uint32_t tn = (uint32_t)ti | 0x80000000u;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        uint32_t v = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          v |= ((int32_t)r[4 * j + c] >= ti ? 1u : 0u) << c;
+          v |= (r[4 * j + c] >= tn ? 1u : 0u) << (4 + c);
+        }
+        nib[j] = v;
+      }
+    } else {
+      // ties at T (count(> T) = chi < x < count(>= T)): keys > T plus the
+      // first x - chi keys == T in index order (chunk, lane, element; R1)
+      const int32_t ti = (int32_t)Tk;
+      const uint32_t tn = Tk | 0x80000000u;
+      int need = (int)((unsigned)x - chi);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        uint32_t g = 0u, eq = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t v = r[4 * j + c];
+          g |= ((int32_t)v > ti ? 1u : 0u) << c;
+          g |= (v > tn ? 1u : 0u) << (4 + c);
+          eq |= (v == (uint32_t)ti ? 1u : 0u) << c;
+          eq |= (v == tn ? 1u : 0u) << (4 + c);
+        }
+        uint32_t e4 = (eq | (eq >> 4)) & 0xfu;      // positions with |u| == T
+        const int ce = __popc(e4);
+        int incl = ce;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int tv = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += tv;
+        }
+        const int take = min(max(need - (incl - ce), 0), ce);
+        while (__popc(e4) > take) e4 &= ~(0x80000000u >> __clz(e4));
+        need -= __shfl_sync(kFull, incl, 31);
+        nib[j] = g | (eq & (e4 | (e4 << 4)));
+      }
+    }
+    // ---- store: lane pairs swap nibbles; even lanes write +, odd lanes - ----
+    {
+      const bool odd = lane & 1;
+      uint8_t* dst = cp + (odd ? pb : 0) + (lane >> 1);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const uint32_t o = __shfl_xor_sync(kFull, nib[j], 1);
+        const uint32_t b = odd ? ((o >> 4) & 0xfu) | (nib[j] & 0xf0u) : (nib[j] & 0xfu) | ((o & 0xfu) << 4);
+        if (FULL || 16 * j + (lane >> 1) < pb) dst[16 * j] = (uint8_t)b;
+      }
+    }
+    if (row + nwarps < n) load_row(up + ustep, raw);
+  }
+}
+
 // Phi^-1(p) for p in (0, 1) (Acklam's rational approximation; only steers the
 // probes of the search, never decides a bit)
 float inv_norm_cdf(double p) {
@@ -809,7 +1032,7 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
     const char* e = getenv("UQ_ENC_DELTA");
     return e ? (float)atof(e) : 0.f;
   }();
-  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.12f : std::is_same<T, __half>::value ? 0.03f : 0.08f);
+  const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.03f : std::is_same<T, __half>::value ? 0.03f : 0.08f);
   if constexpr (std::is_same<T, __half>::value) {
     z0 *= 1.2533141f;   // the f16 kernel steers by mean |u| = s * sqrt(2 / pi) for N(0, s^2)
     if (vec && d == 256 * NCH)
@@ -821,6 +1044,19 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
     else
       encode_f16_kernel<NCH, false, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
           (const __half*)u, n, d, ld, x, z0, delta, codes);
+    note_launch();
+    return cudaGetLastError();
+  }
+  if constexpr (std::is_same<T, float>::value) {
+    if (vec && d == 128 * NCH)
+      encode_f32_kernel<NCH, true, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
+          (const float*)u, n, d, ld, x, z0, delta, codes);
+    else if (vec)
+      encode_f32_kernel<NCH, true, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
+          (const float*)u, n, d, ld, x, z0, delta, codes);
+    else
+      encode_f32_kernel<NCH, false, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
+          (const float*)u, n, d, ld, x, z0, delta, codes);
     note_launch();
     return cudaGetLastError();
   }
