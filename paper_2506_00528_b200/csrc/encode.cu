@@ -822,11 +822,14 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
     ss *= inv_ns;
     const float rms = (ss > 0.f) ? ss * rsqrt_approx(ss) : 0.f;
 
-    // ---- coarse keys: min(top 16 bits of |u|, 0x7bff) as f16 patterns ----
+    // ---- coarse keys: u rounded toward zero to f16 (one F2FP per two elements;
+    // RZ never overflows to inf).  |coarse(u)| >= c <=> |u| >= f16 value c, so
+    // a coarse threshold c is the full-key threshold f32bits(c). ----
     uint32_t cw[NWC];
 #pragma unroll
     for (int i = 0; i < NWC; ++i)
-      cw[i] = h2_bits(__hmin2(__habs2(h2(__byte_perm(r[2 * i], r[2 * i + 1], 0x7632))), h2(0x7bff7bffu)));
+      cw[i] = h2_bits(__halves2half2(__float2half_rz(__uint_as_float(r[2 * i])),
+                                     __float2half_rz(__uint_as_float(r[2 * i + 1]))));
 
     // ---- coarse search: count(>= lo) >= x > count(>= hi) (biased counts) ----
     uint32_t lo = 0u, hi = kCEnd, Tk = 0u;
@@ -835,11 +838,12 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
     float islope;
     {
       const float t = rms * ratio;
-      const uint32_t q1 = __float_as_uint(t * (1.f - delta)) >> 16, q2 = __float_as_uint(t * (1.f + delta)) >> 16;
-      const uint32_t p1 = min(max(q1 & 0x7fffu, 1u), 0x7bfeu);
-      const uint32_t p2 = min(max(q2 & 0x7fffu, p1 + 1u), 0x7bffu);
-      const unsigned n1 = f16_count_ge<NWC, false>(cw, dup16(p1));
-      const unsigned n2 = f16_count_ge<NWC, false>(cw, dup16(p2));
+      const uint32_t pp = __vminu2(__vmaxu2(h2_bits(__floats2half2_rn(t * (1.f - delta), t * (1.f + delta))) & 0x7fff7fffu,
+                                            0x00010001u), 0x7bff7bffu);
+      const uint32_t p1 = pp & 0xffffu;
+      const uint32_t p2 = max(pp >> 16, p1 + 1u);
+      const unsigned n1 = f16_count_ge<NWC>(cw, dup16(p1));
+      const unsigned n2 = f16_count_ge<NWC>(cw, dup16(p2));
       islope = (float)(p2 - p1) * rcp_approx((float)max(n1 - n2, 1u));
       if (n1 == xb) { Tk = p1; exact = true; }
       else if (n2 == xb) { Tk = p2; exact = true; }
@@ -866,7 +870,7 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
           c = min(max(c, lo + 1u), hi - 1u);
           --sec;
         }
-        const unsigned cnt = f16_count_ge<NWC, false>(cw, dup16(c));
+        const unsigned cnt = f16_count_ge<NWC>(cw, dup16(c));
         exact = cnt == xb;
         const bool up_ = cnt > xb;
         Tk = c;
@@ -876,12 +880,13 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
         chi = up_ ? chi : cnt;
       }
     }
+    auto c2key = [](uint32_t c) { return __float_as_uint(__half2float(__ushort_as_half((unsigned short)c))); };
     if (exact) {
-      Tk <<= 16;                      // keys >= Tc << 16 <=> coarse >= Tc: exactly x of them
+      Tk = c2key(Tk);                 // keys >= f32(Tc) <=> coarse >= Tc: exactly x of them
     } else {
-      // ---- full keys inside one coarse value: [lc << 16, hc << 16) ----
+      // ---- full keys inside one coarse value: [f32(lc), f32(hc)) ----
       const unsigned xu = (unsigned)x;
-      uint32_t flo = lo << 16, fhi = (hi == kCEnd) ? 0x80000000u : (hi << 16);
+      uint32_t flo = c2key(lo), fhi = (hi == kCEnd) ? 0x80000000u : c2key(hi);
       unsigned fclo = clo - kF16Bias, fchi = (hi == kCEnd) ? 0u : chi - kF16Bias;
       uint32_t kk[E];
 #pragma unroll
@@ -923,7 +928,29 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
 
     // ---- nibbles (bits 0-3: +1 where u >= T; bits 4-7: -1 where u <= -T) ----
     uint32_t nib[NCH];
-    if (exact || Tk == 0u) {
+    // step(u >= T) = sat((u - Tp) * S) with Tp the float below T and S = 1 /
+    // ulp(Tp) (a power of two; Tp * S is Tp's integer significand, exact):
+    // 0 for u <= Tp, >= 1 before saturation for u >= T (one FFMA rounding).
+    // Nibble bytes are weighted sums 2^23 + sum step * 2^c (exact), whose low
+    // byte is the bit pattern: FMA-pipe work instead of ALU compares.  Needs
+    // Tp normal with biased exponent >= 23 (S <= 2^127); else integer compares.
+    const uint32_t tpb = ((Tk == 0u) ? 1u : Tk) - 1u;
+    const uint32_t tpe = tpb >> 23;
+    if ((exact || Tk == 0u) && tpe >= 23u && tpe <= 254u) {
+      const float S = __uint_as_float((277u - tpe) << 23);
+      const float nts = -__uint_as_float(tpb) * S;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        float acc = 8388608.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float v = __uint_as_float(r[4 * j + c]);
+          acc = fmaf(__saturatef(fmaf(v, S, nts)), (float)(1 << c), acc);
+          acc = fmaf(__saturatef(fmaf(-v, S, nts)), (float)(16 << c), acc);
+        }
+        nib[j] = __float_as_uint(acc);   // low byte: + bits 0-3, - bits 4-7
+      }
+    } else if (exact || Tk == 0u) {
       const int32_t ti = (int32_t)((Tk == 0u) ? 1u : Tk);
       const uint32_t tn = (uint32_t)ti | 0x80000000u;
 #pragma unroll

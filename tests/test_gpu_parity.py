@@ -97,6 +97,49 @@ def test_encode_extreme_distributions(uq, orc, dt):
         assert bad.size == 0, (dt, x, bad, bad % 7)
 
 
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16])
+def test_encode_threshold_boundaries(uq, orc, dt):
+    """T* placed on the encoders' internal boundaries: row scales 2^k sweeping
+    the whole exponent range (f32: the f16 coarse keys underflow / saturate and
+    the FMA-pipe selection's S = 1/ulp(T-) leaves its range below 2^-104; f16:
+    subnormal thresholds), magnitudes that are exact powers of two (T* on a
+    binade edge, massive ties), values one f32 ulp apart inside one coarse value
+    (the full-key phase), and values at / beyond the f16 maximum."""
+    rng = np.random.default_rng(23)
+    d = 768
+    rows = []
+    if dt == torch.float32:
+        scales = [-149, -140, -130, -127, -126, -120, -110, -106, -105, -104, -103, -102, -100, -60, -24, -15,
+                  -14, 0, 15, 16, 17, 40, 100, 120, 124]
+    else:
+        scales = [-24, -22, -20, -16, -15, -14, -13, -10, 0, 5, 10, 12, 13]
+    for k in scales:
+        for _ in range(3):
+            rows.append(rng.standard_normal(d) * 2.0 ** k)
+    for _ in range(12):
+        rows.append(np.sign(rng.standard_normal(d)) * 2.0 ** rng.integers(-3, 4, d))      # binade edges, ties
+    if dt == torch.float32:
+        one = np.float32(1.0)
+        for _ in range(12):                                   # one f32 ulp apart, one coarse value
+            steps = rng.integers(0, 40, d).astype(np.float32)
+            rows.append(np.sign(rng.standard_normal(d)) * (one + steps * np.float32(2.0 ** -23)))
+        for _ in range(6):                                    # at / beyond the f16 maximum (coarse clamp)
+            rows.append(np.sign(rng.standard_normal(d)) * (65504.0 + rng.integers(0, 64, d).astype(np.float64)))
+    else:
+        for _ in range(6):
+            rows.append(np.sign(rng.standard_normal(d)) * (65504.0 - 32.0 * rng.integers(0, 4, d)))
+    host = np.stack(rows).astype(np.float32)
+    if dt == torch.float32:
+        host = np.clip(host, -3.0e38, 3.0e38)
+    ut = torch.from_numpy(host).to(dt)
+    ref_in = ut.numpy() if dt == torch.float16 else ut.numpy()
+    for x in (1, 2, 200, 384, 383, 767, 768):
+        got = uq.encode(ut.cuda(), x).cpu().numpy()
+        ref = orc.pack(orc.encode(ref_in, x))
+        bad = np.argwhere((got != ref).any(1))[:5].ravel()
+        assert bad.size == 0, (dt, x, bad)
+
+
 def test_encode_strided_and_table3(uq, orc):
     import json, os
     t = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table3_p356.json")))
