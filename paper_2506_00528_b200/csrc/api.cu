@@ -211,7 +211,12 @@ static SearchLayout layout_for(uq_algo a, int64_t nq, int64_t n, int32_t d, int3
   L.part_off = bufs;
   L.cnt_off = L.part_off + part;      // [lists][nq] valid entries per list (pair engine)
   const int op = pair_op(a, nq, d);
-  const size_t cnt_bytes = op >= 0 ? align_up((size_t)plan_tc2(nq, n, d, k, sms, op).n_chunks * nq * 4, 256) : 0;
+  size_t cnt_bytes = op >= 0 ? align_up((size_t)plan_tc2(nq, n, d, k, sms, op).n_chunks * nq * 4, 256) : 0;
+  if (!is_tc(a)) {   // the popcount scan publishes counted lists too
+    int64_t ch = plan_popc(nq, n, d, k, sms).n_chunks;
+    if (sp.on && !hist) ch = std::max<int64_t>(ch, plan_popc(nq, sp.rows, d, k, sms).n_chunks);
+    cnt_bytes = align_up((size_t)ch * nq * 4, 256);
+  }
   L.seed_s_off = L.cnt_off + cnt_bytes;   // top-k seed: [nq][k] scores; hist seed: [nq] bounds
   L.seed_i_off = L.seed_s_off + (sp.on ? align_up((size_t)nq * (hist ? 1 : k) * 4, 256) : 0);
   L.hist_off = L.seed_i_off + (sp.on && !hist ? align_up((size_t)nq * k * 8, 256) : 0);
@@ -248,14 +253,15 @@ static cudaError_t scan_and_merge(uq_algo a, const uint8_t* q, int64_t nq, const
     lists = tp.n_chunks;
   } else {
     const PopcPlan pl = plan_popc(nq, n, d, k, sms);
-    e = launch_scan_popc(q, nq, db, n, d, k, pl, bufs, part, thr0, thr0_stride, row_stride, st);
+    e = launch_scan_popc(q, nq, db, n, d, k, pl, bufs, part, thr0, thr0_stride, row_stride, st, part_cnt);
     lists = pl.n_chunks;
   }
   timer_end(st, ev);
   if (e != cudaSuccess) return e;
-  // the pair engine publishes variable-length lists of up to cap entries with counts
-  const bool counted = op >= 0;
-  const int32_t kin = counted ? plan_tc2(nq, n, d, k, sms, op).cap : k;
+  // the pair engine publishes variable-length lists of up to cap entries with
+  // counts, the popcount scan lists of up to k entries with counts
+  const bool counted = op >= 0 || !is_tc(a);
+  const int32_t kin = op >= 0 ? plan_tc2(nq, n, d, k, sms, op).cap : k;
   return launch_merge_keys(part, lists, nq, kin, k, id_base, out_s, out_id, st, counted ? part_cnt : nullptr, qfail,
                            any, mscr, mscr_bytes);
 }

@@ -59,7 +59,7 @@ PopcPlan plan_popc(int64_t nq, int64_t n, int32_t d, int32_t k, int sms);
 cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                              int32_t k, const PopcPlan& pl, uint32_t* bufs, uint64_t* part,
                              const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
-                             cudaStream_t st);
+                             cudaStream_t st, int32_t* part_cnt = nullptr);
 
 // Tensor-core scan (scan_tc.cu).
 struct TcPlan {

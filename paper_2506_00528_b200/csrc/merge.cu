@@ -159,9 +159,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
       s_hist[threadIdx.x] = 0u;
       __syncthreads();
       const uint64_t hi = shr64(prefix, r);
-      for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) {
-        const uint64_t key = get(i);
-        if (key != 0ull && shr64(key, r) == hi) atomicAdd(&s_hist[(unsigned)(key >> sh) & dmask], 1u);
+      // warp-aggregated: candidates concentrate in a few digits (seeded scans
+      // keep only scores near D_k), so lanes with equal digits add once
+      // (MATCH + POPC) instead of serialising on one shared-memory word
+      for (int64_t b = (int64_t)warp * 32; b < C; b += kMergeThreads) {
+        const int64_t i = b + lane;
+        const uint64_t key = i < C ? get(i) : 0ull;
+        const bool in = key != 0ull && shr64(key, r) == hi;
+        const unsigned bin = in ? ((unsigned)(key >> sh) & dmask) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(kFull, bin);
+        if (in && (peers & ((1u << lane) - 1u)) == 0u) atomicAdd(&s_hist[bin], (unsigned)__popc(peers));
       }
       __syncthreads();
       if (warp == 0) {
@@ -200,12 +207,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
     T = prefix;
   }
   // (2) gather the keys >= T (exactly min(k, nvalid): keys are unique)
-  for (int64_t i = threadIdx.x; i < C; i += kMergeThreads) {
-    const uint64_t key = get(i);
-    if (key != 0ull && key >= T) {
-      const int pos = atomicAdd(&s_nsel, 1);
-      if (pos < P) s_sel[pos] = key;
-    }
+  for (int64_t b = (int64_t)warp * 32; b < C; b += kMergeThreads) {   // one atomic per warp
+    const int64_t i = b + lane;
+    const uint64_t key = i < C ? get(i) : 0ull;
+    const bool take = key != 0ull && key >= T;
+    const unsigned m = __ballot_sync(kFull, take);
+    int base = 0;
+    if (lane == 0 && m != 0u) base = atomicAdd(&s_nsel, __popc(m));
+    base = __shfl_sync(kFull, base, 0);
+    const int pos = base + __popc(m & ((1u << lane) - 1u));
+    if (take && pos < P) s_sel[pos] = key;
   }
   __syncthreads();
   const int nsel = s_nsel < p.k ? s_nsel : p.k;
@@ -225,17 +236,20 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeParams p) {
   }
 }
 
-static int merge_smem(int32_t k, int64_t C, int32_t* stage_cap) {
+static int merge_smem(int32_t k, int64_t C, int32_t* stage_cap, int64_t bytes) {
   const int P = 1 << bitlen((unsigned)(k - 1 > 0 ? k - 1 : 1));
-  const int64_t budget = 48 * 1024 / 8 - P;  // keys staged beside s_sel (4 CTAs per SM)
+  const int64_t budget = bytes / 8 - P;  // keys staged beside s_sel
   *stage_cap = (int32_t)(C <= budget ? C : budget);   // lists larger than this are read from global
   return (int)((P + *stage_cap) * 8);
 }
 
-static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t st, unsigned groups = 1) {
+// smem_bytes: staging budget (48 KB: 4 CTAs per SM; a few-query merge with one
+// CTA per query takes most of an SM's shared memory instead)
+static cudaError_t launch_merge_common(MergeParams p, bool from_si, cudaStream_t st, unsigned groups = 1,
+                                       int64_t smem_bytes = 48 * 1024) {
   if (p.nq <= 0) return cudaSuccess;
   const int64_t lists_per_cta = (!from_si && p.lpg > 0) ? p.lpg : p.lists;
-  const int smem = merge_smem(p.k, lists_per_cta * p.kin, &p.stage_cap);
+  const int smem = merge_smem(p.k, lists_per_cta * p.kin, &p.stage_cap, smem_bytes);
   const dim3 grid((unsigned)p.nq, groups);
   if (from_si) {
     cudaError_t e = cudaFuncSetAttribute(merge_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

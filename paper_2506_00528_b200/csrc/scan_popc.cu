@@ -57,6 +57,7 @@ struct PopcParams {
   int32_t thr0_stride;
   int64_t row_stride;   // DB row r of this scan is row r * row_stride of dbcodes
   int32_t check;        // stages between stream checks (popc_check)
+  int32_t* part_cnt;    // optional [S][nq]: valid entries per published list (the rest is left unwritten)
 };
 
 // Delta of this lane's DB row (dm = r+ | r-, dn = r-) against every query of
@@ -177,8 +178,10 @@ __global__ void __launch_bounds__(kScanThreads, OCC) scan_popc_kernel(PopcParams
       uint32_t* buf = mybufs + (size_t)j * p.cap;
       if (cnt > p.k) { stream_rebuild(buf, cnt, p.k, lane); cnt = p.k; }
       uint64_t* out = p.part + ((size_t)c * p.nq + (q0 + j)) * p.k;
-      for (int i = lane; i < p.k; i += 32)
+      const int wr = p.part_cnt != nullptr ? cnt : p.k;   // counted lists: no zero padding
+      for (int i = lane; i < wr; i += 32)
         out[i] = (i < cnt) ? global_key_from_local(p.kf, buf[i], (uint64_t)row0) : 0ull;
+      if (p.part_cnt != nullptr && lane == 0) p.part_cnt[(size_t)c * p.nq + (q0 + j)] = cnt;
     }
   }
 }
@@ -341,8 +344,10 @@ scan_popc_tma_kernel(const __grid_constant__ CUtensorMap tmap, PopcParams p, int
       uint32_t* buf = mybufs + (size_t)j * p.cap;
       if (cnt > p.k) { stream_rebuild(buf, cnt, p.k, lane); cnt = p.k; }
       uint64_t* out = p.part + ((size_t)c * p.nq + (q0 + j)) * p.k;
-      for (int i = lane; i < p.k; i += 32)
+      const int wr = p.part_cnt != nullptr ? cnt : p.k;   // counted lists: no zero padding
+      for (int i = lane; i < wr; i += 32)
         out[i] = (i < cnt) ? global_key_from_local(p.kf, buf[i], (uint64_t)row0) : 0ull;
+      if (p.part_cnt != nullptr && lane == 0) p.part_cnt[(size_t)c * p.nq + (q0 + j)] = cnt;
     }
   }
 }
@@ -463,9 +468,9 @@ static cudaError_t launch_popc_nb(const PopcParams& p, const PopcPlan& pl, cudaS
 cudaError_t launch_scan_popc(const uint8_t* q, int64_t nq, const uint8_t* db, int64_t n, int32_t d,
                              int32_t k, const PopcPlan& pl, uint32_t* bufs, uint64_t* part,
                              const int32_t* thr0, int32_t thr0_stride, int64_t row_stride,
-                             cudaStream_t st) {
+                             cudaStream_t st, int32_t* part_cnt) {
   PopcParams p{q, nq, db, n, d, k, make_keyfmt(d), pl.qt, pl.n_qtiles, pl.n_chunks, pl.L, pl.cap,
-               bufs, part, thr0, thr0_stride, row_stride, popc_check(k)};
+               bufs, part, thr0, thr0_stride, row_stride, popc_check(k), part_cnt};
   switch (blocks128(d)) {
 #define UQ_POPC_CASE(N) \
   case N: return launch_popc_nb<N>(p, pl, st);
