@@ -157,6 +157,27 @@ def test_encode_strided_and_table3(uq, orc):
         assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("d", [128, 384, 768, 1024])
+def test_encode_f16_row_pairs(uq, orc, d):
+    """fp16 rows with d = 128k run two rows per warp (one per half-warp): odd
+    and even row counts (the odd row out is duplicated, not stored), tiny n,
+    and neighbouring rows of very different kinds so the two halves of a warp
+    take different search paths (exact / ties / T* = 0 / extrapolation)."""
+    rng = np.random.default_rng(d + 5)
+    for n in (1, 2, 3, 17, 1000):
+        u = rng.standard_normal((n, d)).astype(np.float32)
+        u[1::4] = _tie_heavy(rng, len(u[1::4]), d)
+        u[2::4] *= np.float32(1e-3) ** rng.integers(0, 3, (len(u[2::4]), 1))
+        u[3::8] = 0.0
+        u[3::8, ::5] = 1.0
+        ut = torch.from_numpy(u).to(torch.float16)
+        for x in sorted({1, d // 3, d // 2, d - 1, d}):
+            got = uq.encode(ut.cuda(), x).cpu().numpy()
+            ref = orc.pack(orc.encode(ut.numpy(), x))
+            bad = np.argwhere((got != ref).any(1))[:5].ravel()
+            assert bad.size == 0, (d, n, x, bad)
+
+
 def test_encode_c5_fp16_unnormalised(uq, orc):
     """Config 5 recipe (fp16, raw mixture values; ~10% of rows tie at the top-x boundary)."""
     w = datagen.CONFIGS["c5"].scaled(n=20000, nq=16)
