@@ -75,6 +75,14 @@ __device__ __forceinline__ uint32_t local_key(const KeyFmt& f, int32_t delta, ui
   return ((uint32_t)(delta + f.off) << f.rb) | (f.rmask - local_row);
 }
 
+// base[i] = v where p, as one predicated store (no branch, no reconvergence);
+// the address is one wide multiply-add of the 32-bit index
+__device__ __forceinline__ void st_global_if(uint32_t* base, uint32_t i, uint32_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\t.reg .u64 a;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+               "mad.wide.u32 a, %1, 4, %0;\n\t@q st.global.u32 [a], %2;\n\t}"
+               ::"l"(base), "r"(i), "r"(v), "r"((uint32_t)p) : "memory");
+}
+
 __device__ __forceinline__ uint64_t global_key_from_local(const KeyFmt& f, uint32_t lk, uint64_t chunk_start) {
   if (lk == 0) return 0ull;
   int32_t delta = (int32_t)(lk >> f.rb) - f.off;

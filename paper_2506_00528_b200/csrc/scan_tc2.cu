@@ -769,19 +769,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
             const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                         max(cm[6], cm[7]));
             if (__any_sync(kFull, mx > thb)) {
-              const uint32_t rb0 = (uint32_t)(lr0 + c0);
+              // rmask - local row of column 4i + j is rk0 - 4i - j
+              const uint32_t rk0 = p.kf.rmask - (uint32_t)(lr0 + c0);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 if (__any_sync(kFull, cm[i] > thb)) {
+                  // predicated appends, no branches: the 4 keys are built
+                  // unconditionally and stored where the score passes (a
+                  // divergent branch per score cost ~67 instructions and four
+                  // reconvergence regions per chunk; with k = 100 about half of
+                  // the 32-score groups of a warp take this path)
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const int sc = (int)v[4 * i + j];
-                    if (sc > thb) {
-                      const int dv = OP != kOpF4 ? sc : raw ? __float2int_rn(__int_as_float(sc)) : sc - kF4Bias;
-                      UQ_ASSERT(cnt < p.cap);
-                      my_buf[cnt++] = local_key(p.kf, dv, rb0 + (uint32_t)(4 * i + j));
-                      ++n_app;
-                    }
+                    const bool pj = sc > thb;
+                    // Delta + off: int8 scores directly; f32 scores through the
+                    // biased pattern kF4Bias + Delta (raw tiles add 1.5 * 2^23
+                    // here: one FADD instead of an F2I on the XU pipe)
+                    const int dvo = OP != kOpF4 ? sc + p.kf.off
+                                    : (raw ? __float_as_int(__int_as_float(sc) + 12582912.0f) : sc) + (p.kf.off - kF4Bias);
+                    const uint32_t key = ((uint32_t)dvo << p.kf.rb) | (rk0 - (uint32_t)(4 * i + j));
+                    UQ_ASSERT(!pj || cnt < p.cap);
+                    st_global_if(my_buf, (uint32_t)cnt, key, pj);
+                    cnt += pj ? 1 : 0;
+                    if (PROF_ON) n_app += pj ? 1u : 0u;
                   }
                 }
               }

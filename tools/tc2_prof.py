@@ -21,6 +21,8 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else None
 nq = int(sys.argv[3]) if len(sys.argv) > 3 else None
 w = datagen.CONFIGS[cfg].scaled(n=n, nq=nq)
+if os.environ.get("UQ_PROF_K"):
+    w = w.scaled(k=int(os.environ["UQ_PROF_K"]))
 db = uq.encode(datagen.db(w, "cuda"), w.x)
 q = uq.encode(datagen.queries(w, "cuda"), w.x)
 MODE = os.environ.get("UQ_PROF_ALGO", "f4")   # f4 | tc | asym
