@@ -769,8 +769,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
             const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                         max(cm[6], cm[7]));
             if (__any_sync(kFull, mx > thb)) {
-              // rmask - local row of column 4i + j is rk0 - 4i - j
-              const uint32_t rk0 = p.kf.rmask - (uint32_t)(lr0 + c0);
+              // key = ((Delta + off) << rb) | (rmask - local row), written as
+              // (s << rb) + kb0 - (4i + j): s = the score as an integer
+              // pattern (int8: Delta; f32: kF4Bias + Delta, from one FADD
+              // whose addend is 1.5 * 2^23 on raw tiles and 0 on biased ones,
+              // which already hold that pattern), kb0 folds the pattern bias,
+              // off and the row term (shifts distribute over + mod 2^32; the
+              // row term stays below 2^rb, so + is the |)
+              const uint32_t kb0 = ((uint32_t)(OP != kOpF4 ? p.kf.off : p.kf.off - kF4Bias) << p.kf.rb) +
+                                   (p.kf.rmask - (uint32_t)(lr0 + c0));
+              const float fadd = raw ? 12582912.0f : 0.0f;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 if (__any_sync(kFull, cm[i] > thb)) {
@@ -783,12 +791,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
                   for (int j = 0; j < 4; ++j) {
                     const int sc = (int)v[4 * i + j];
                     const bool pj = sc > thb;
-                    // Delta + off: int8 scores directly; f32 scores through the
-                    // biased pattern kF4Bias + Delta (raw tiles add 1.5 * 2^23
-                    // here: one FADD instead of an F2I on the XU pipe)
-                    const int dvo = OP != kOpF4 ? sc + p.kf.off
-                                    : (raw ? __float_as_int(__int_as_float(sc) + 12582912.0f) : sc) + (p.kf.off - kF4Bias);
-                    const uint32_t key = ((uint32_t)dvo << p.kf.rb) | (rk0 - (uint32_t)(4 * i + j));
+                    const uint32_t sp = OP != kOpF4 ? (uint32_t)sc : __float_as_uint(__int_as_float(sc) + fadd);
+                    const uint32_t key = (sp << p.kf.rb) + (kb0 - (uint32_t)(4 * i + j));
                     UQ_ASSERT(!pj || cnt < p.cap);
                     st_global_if(my_buf, (uint32_t)cnt, key, pj);
                     cnt += pj ? 1 : 0;
