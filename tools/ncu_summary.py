@@ -97,7 +97,11 @@ def lines(rep, top):
               f"{dict(st[k].most_common(2))} | {src[k]}")
 
 
-def launches(path):
+OURS = ("uq::", "tc2::", "encode_", "scan_", "merge_kernel", "rerank_", "quantize", "build_", "thr_from",
+        "seed_verify", "check_codes", "scores_kernel")
+
+
+def launches(path, ours=False):
     rows = list(csv.reader(open(path)))
     hdr = None
     agg = collections.defaultdict(list)
@@ -113,6 +117,8 @@ def launches(path):
                     v /= 1e3
                 elif d["Metric Unit"] in ("msecond", "ms"):
                     v *= 1e3
+                if ours and not any(t in d["Kernel Name"] for t in OURS):
+                    continue   # data generation / recall ground truth (torch, cuBLAS)
                 agg[(d["Kernel Name"][:70], d["Grid Size"])].append(v)
     tot = sum(sum(v) for v in agg.values())
     print(f"{'kernel':70s} {'grid':>14s} {'n':>4s} {'mean_us':>10s} {'share':>6s}")
@@ -123,7 +129,7 @@ def launches(path):
 if __name__ == "__main__":
     a = sys.argv[1:]
     if a and a[0] == "--launches":
-        launches(a[1])
+        launches(a[1], ours="--ours" in a)
     else:
         top = int(a[a.index("--lines") + 1]) if "--lines" in a else 0
         raw(a[0])
