@@ -673,17 +673,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<OP>::threads(MOD
             const int mx = __vimax3_s32(__vimax3_s32(cm[0], cm[1], cm[2]), __vimax3_s32(cm[3], cm[4], cm[5]),
                                         max(cm[6], cm[7]));
             if (__any_sync(kFull, mx > fl)) {
+              // predicated histogram increments, no branch per score (as the
+              // top-k appends): Delta from one FADD whose addend is 1.5 * 2^23
+              // on raw tiles and 0 on biased ones
+              const float fadd = raw ? 12582912.0f : 0.0f;
+              const uint32_t hbase = smem_u32(s_hist) + 4u * (uint32_t)col;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 if (__any_sync(kFull, cm[i] > fl)) {
 #pragma unroll
                   for (int j = 0; j < 4; ++j) {
                     const int sc = (int)v[4 * i + j];
-                    if (sc > fl) {
-                      const int dv = OP != kOpF4 ? sc : raw ? __float2int_rn(__int_as_float(sc)) : sc - kF4Bias;
-                      const uint32_t b = min((uint32_t)(dv - floor_m1 - 1) >> hs_q, (uint32_t)(kHistBins - 1));
-                      atomicAdd(s_hist + (b >> 1) * BM + col, (b & 1u) ? 0x10000u : 1u);
-                    }
+                    const int dv = OP != kOpF4 ? sc : __float_as_int(__int_as_float(sc) + fadd) - kF4Bias;
+                    const uint32_t b = min((uint32_t)(dv - floor_m1 - 1) >> hs_q, (uint32_t)(kHistBins - 1));
+                    red_shared_add_if(hbase + (b >> 1) * (4u * BM), (b & 1u) ? 0x10000u : 1u, sc > fl);
                   }
                 }
               }
