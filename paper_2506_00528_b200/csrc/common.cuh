@@ -83,6 +83,11 @@ __device__ __forceinline__ void st_global_if(uint32_t* base, uint32_t i, uint32_
                ::"l"(base), "r"(i), "r"(v), "r"((uint32_t)p) : "memory");
 }
 
+// *ptr += v where p, one predicated global reduction (no branch)
+__device__ __forceinline__ void red_global_add_if(uint32_t* ptr, uint32_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.u32 [%0], %1;\n\t}"
+               ::"l"(ptr), "r"(v), "r"((uint32_t)p) : "memory");
+}
 // shared [addr] += v where p, one predicated reduction (no branch)
 __device__ __forceinline__ void red_shared_add_if(uint32_t addr, uint32_t v, bool p) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}"

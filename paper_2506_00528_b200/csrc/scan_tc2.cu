@@ -200,11 +200,15 @@ template <int HB>
 __device__ __forceinline__ void hist_flush(uint32_t* s_hist, int col, uint32_t* g) {
 #pragma unroll 4
   for (int w = 0; w < HB / 2; ++w) {
+    // the flush runs between two named barriers of every set of this
+    // quarter: plain load + store, and predicated global reductions for the
+    // (few) non-zero bins instead of a divergent branch per bin
     uint32_t* cell = s_hist + w * BM + col;
-    const uint32_t v = atomicExch(cell, 0u);
+    const uint32_t v = *cell;
+    *cell = 0u;
     if (g != nullptr) {   // (timing ablation UQ_TC_ABLATE & 64 passes g = nullptr)
-      if (v & 0xffffu) atomicAdd(g + 2 * w, v & 0xffffu);
-      if (v >> 16) atomicAdd(g + 2 * w + 1, v >> 16);
+      red_global_add_if(g + 2 * w, v & 0xffffu, (v & 0xffffu) != 0u);
+      red_global_add_if(g + 2 * w + 1, v >> 16, (v >> 16) != 0u);
     }
   }
 }
