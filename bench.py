@@ -746,8 +746,11 @@ def _extras(c: Ctx, args):
                    "digest": r["digest"]["all"]}
         enc = r["encode"]
         ex[key]["encode"] = {kk: enc[kk] for kk in ("GB_per_s", "hbm_frac", "ms", "timing")}
-        # end to end for the config: encode the whole fp16 DB, then one batch
-        ex[key]["e2e_db_encode_plus_batch_ms"] = enc["ms"] + r["ms_per_step"]
+        # end to end for the config: encode the whole fp16 DB, build the E2M1
+        # index when the batch's engine reads one, then one batch
+        idx_ms = (r.get("index") or {}).get("f4_index_build_ms") or 0.0
+        ex[key]["f4_index_build_ms"] = idx_ms
+        ex[key]["e2e_db_encode_plus_batch_ms"] = enc["ms"] + idx_ms + r["ms_per_step"]
     del db5
     torch.cuda.empty_cache()
     return ex
