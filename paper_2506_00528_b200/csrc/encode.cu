@@ -34,6 +34,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 
@@ -617,13 +619,19 @@ __device__ __forceinline__ float rsqrt_approx(float v) {
 #ifndef UQ_ENC16_EMA
 #define UQ_ENC16_EMA 0.15f
 #endif
+#ifndef UQ_ENC16_ONEPROBE
+#define UQ_ENC16_ONEPROBE 1
+#endif
+#ifndef UQ_ENC16_SLOPE_EMA
+#define UQ_ENC16_SLOPE_EMA 0.05f
+#endif
 #ifndef UQ_ENC16_REDUX_SCALE
 #define UQ_ENC16_REDUX_SCALE 1
 #endif
 template <int NCH, bool VECLOAD, bool FULL>
 __global__ void __launch_bounds__(kEncWarps * 32, NCH <= 4 ? 6 : 3)
 encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t x, float z0, float delta,
-                  uint8_t* __restrict__ codes) {
+                  float slope0, uint8_t* __restrict__ codes) {
   constexpr int NW = 4 * NCH;                 // half pairs per lane
   constexpr int NS = NCH < 2 ? NCH : 2;       // chunks sampled for the RMS
   constexpr uint32_t kEnd = 0x7c01u;          // finite keys are < kEnd (inf / NaN: precondition, R4)
@@ -636,6 +644,7 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
   const unsigned xb = (unsigned)x + kF16Bias;
   const int64_t ustep = nwarps * ld, cstep = nwarps * cb;
   float ratio = z0;   // T* / RMS, averaged over this warp's rows
+  float slope = slope0;   // keys per unit of count near T*, averaged over this warp's rows
   auto load_row = [&](const __half* src, uint4 (&r)[NCH]) {
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
@@ -685,6 +694,58 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
     uint32_t lo = 0u, hi = kEnd, Tk = 0u;
     unsigned clo = 256u * NCH + kF16Bias, chi = kF16Bias;
     bool exact = false;
+#if UQ_ENC16_ONEPROBE
+    // one probe at the predicted T*, then a step by the warp's learned count
+    // slope straight at the x-th count (a simulator of this search on c5 rows:
+    // 4.82 -> 4.05 count passes per row against two probes at t(1 -/+ delta))
+    uint32_t p1;
+    unsigned n1;
+    {
+      const float t = rms * ratio;
+      p1 = min(max((uint32_t)__half_as_ushort(__float2half_rn(t)) & 0x7fffu, 1u), 0x7bffu);
+      n1 = f16_count_ge<NW>(w, dup16(p1));
+      float islope = slope;
+      uint32_t c = p1;
+      if (n1 == xb) { Tk = p1; exact = true; }
+      else {
+        const bool up1 = n1 > xb;
+        lo = up1 ? p1 : 0u; clo = up1 ? n1 : clo;
+        hi = up1 ? kEnd : p1; chi = up1 ? chi : n1;
+        // n1 - xb > 0: T* above p1; the step lands inside (lo, hi)
+        c = (uint32_t)((int)p1 + __float2int_rn((float)(int)(n1 - xb) * slope));
+        c = (int)c <= (int)lo ? lo + 1u : min(c, hi - 1u);
+      }
+      unsigned sec = 6u;   // interpolated passes before the forced bisections start
+#pragma unroll 1
+      while (!exact) {
+        const unsigned cnt = f16_count_ge<NW>(w, dup16(c));
+        exact = cnt == xb;
+        const bool up_ = cnt > xb;
+        Tk = c;
+        lo = up_ ? c : lo;
+        clo = up_ ? cnt : clo;
+        hi = up_ ? hi : c;
+        chi = up_ ? chi : cnt;
+        if (exact || hi - lo <= 1u) break;
+        if (hi == kEnd || lo == 0u) {
+          // T* still outside the bracket: step past its one end by the
+          // learned slope, doubling each time the step falls short
+          const uint32_t s = (uint32_t)(((float)(hi == kEnd ? clo - xb : xb - chi) + 0.5f) * islope) + 1u;
+          c = hi == kEnd ? lo + s : (hi > s ? hi - s : 0u);
+          c = min(max(c, lo + 1u), hi - 1u);
+          islope *= 2.f;
+        } else if (sec == 0u) {
+          c = lo + ((hi - lo) >> 1);                 // guaranteed progress
+          sec = 1u;
+        } else {
+          const float f = ((float)(clo - xb) + UQ_ENC16_OFF) * rcp_approx((float)(clo - chi));
+          c = lo + (uint32_t)(f * (float)(hi - lo));
+          c = min(max(c, lo + 1u), hi - 1u);
+          --sec;
+        }
+      }
+    }
+#else
     float islope;
     {
       const float t = rms * ratio;
@@ -734,11 +795,18 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
       hi = up_ ? hi : c;
       chi = up_ ? chi : cnt;
     }
+#endif
     if (!exact) { Tk = lo; exact = (clo == xb); }
     if (Tk != 0u && rms > 0.f) {
       const float rn = __fdividef(ElemBits<__half>::key2f(Tk), rms);
       if (rn > 0.f && rn < 1e30f) ratio = fmaf(UQ_ENC16_EMA, rn - ratio, ratio);
     }
+#if UQ_ENC16_ONEPROBE
+    if (n1 != xb) {   // observed keys per count between the probe and T*
+      const float so = (float)abs((int)Tk - (int)p1) * rcp_approx((float)abs((int)(n1 - xb)));
+      slope = fmaf(UQ_ENC16_SLOPE_EMA, min(so, 4096.f) - slope, slope);
+    }
+#endif
 
     // ---- plane bytes: +1 where u >= T, -1 where u <= -T (T >= 1: zeros never) ----
     uint32_t posb[NCH], negb[NCH];
@@ -1097,16 +1165,21 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
   }();
   const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.03f : std::is_same<T, __half>::value ? 0.03f : 0.08f);
   if constexpr (std::is_same<T, __half>::value) {
+    // initial keys per unit of count near T* for d half-normal magnitudes of
+    // scale s: count density 2 d phi(z) / s per unit value, ~T* 2^-10.5 per
+    // key (f16 ulp) at T* = s z -> 2^10.5 / (2 d phi(z) z); learned per warp
+    const double phz = std::exp(-0.5 * (double)z0 * (double)z0) * 0.3989422804014327;
+    const float slope0 = (float)std::min(4096.0, std::max(0.25, 1448.15468787 / (2.0 * d * phz * (double)z0)));
     z0 *= 1.2533141f;   // the f16 kernel steers by mean |u| = s * sqrt(2 / pi) for N(0, s^2)
     if (vec && d == 256 * NCH)
       encode_f16_kernel<NCH, true, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-          (const __half*)u, n, d, ld, x, z0, delta, codes);
+          (const __half*)u, n, d, ld, x, z0, delta, slope0, codes);
     else if (vec)
       encode_f16_kernel<NCH, true, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-          (const __half*)u, n, d, ld, x, z0, delta, codes);
+          (const __half*)u, n, d, ld, x, z0, delta, slope0, codes);
     else
       encode_f16_kernel<NCH, false, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-          (const __half*)u, n, d, ld, x, z0, delta, codes);
+          (const __half*)u, n, d, ld, x, z0, delta, slope0, codes);
     note_launch();
     return cudaGetLastError();
   }
