@@ -882,7 +882,7 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
 template <int NCH, bool VECLOAD, bool FULL>
 __global__ void __launch_bounds__(kEncWarps * 32, NCH > 8 ? 2 : 3)
 encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld, int32_t x, float z0, float delta,
-                  uint8_t* __restrict__ codes) {
+                  float slope0, uint8_t* __restrict__ codes) {
   constexpr int E = 4 * NCH;                  // elements per lane
   constexpr int NWC = 2 * NCH;                // coarse half pairs per lane
   constexpr int NS = NCH < 2 ? NCH : NCH / 2; // chunks sampled for the RMS
@@ -896,6 +896,7 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
   const unsigned xb = (unsigned)x + kF16Bias;
   const int64_t ustep = nwarps * ld, cstep = nwarps * cb;
   float ratio = z0;   // T* / RMS, averaged over this warp's rows
+  float slope = slope0;   // coarse keys per unit of count near T*, averaged over this warp's rows
   auto load_row = [&](const float* src, uint4 (&r)[NCH]) {
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
@@ -939,6 +940,59 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
     uint32_t lo = 0u, hi = kCEnd, Tk = 0u;
     unsigned clo = 128u * NCH + kF16Bias, chi = kF16Bias;
     bool exact = false;
+#if UQ_ENC16_ONEPROBE
+    // one probe at the predicted T*, then a step by the warp's learned slope
+    // (as the f16 kernel)
+    uint32_t p1;
+    unsigned n1;
+    {
+      p1 = min(max((uint32_t)__half_as_ushort(__float2half_rn(rms * ratio)) & 0x7fffu, 1u), 0x7bffu);
+      n1 = f16_count_ge<NWC>(cw, dup16(p1));
+      float islope = slope;
+      uint32_t c = p1;
+      if (n1 == xb) { Tk = p1; exact = true; }
+      else {
+        const bool up1 = n1 > xb;
+        lo = up1 ? p1 : 0u; clo = up1 ? n1 : clo;
+        hi = up1 ? kCEnd : p1; chi = up1 ? chi : n1;
+        c = (uint32_t)((int)p1 + __float2int_rn((float)(int)(n1 - xb) * slope));
+        c = (int)c <= (int)lo ? lo + 1u : min(c, hi - 1u);
+      }
+      unsigned sec = 6u;
+#pragma unroll 1
+      while (!exact) {
+        const unsigned cnt = f16_count_ge<NWC>(cw, dup16(c));
+        exact = cnt == xb;
+        const bool up_ = cnt > xb;
+        Tk = c;
+        lo = up_ ? c : lo;
+        clo = up_ ? cnt : clo;
+        hi = up_ ? hi : c;
+        chi = up_ ? chi : cnt;
+        if (exact || hi - lo <= 1u) break;
+        if (hi == kCEnd || lo == 0u) {
+          const uint32_t s = (uint32_t)(((float)(hi == kCEnd ? clo - xb : xb - chi) + 0.5f) * islope) + 1u;
+          c = hi == kCEnd ? lo + s : (hi > s ? hi - s : 0u);
+          c = min(max(c, lo + 1u), hi - 1u);
+          islope *= 2.f;
+        } else if (sec == 0u) {
+          c = lo + ((hi - lo) >> 1);
+          sec = 1u;
+        } else {
+          const float f = ((float)(clo - xb) + 0.5f) * rcp_approx((float)(clo - chi));
+          c = lo + (uint32_t)(f * (float)(hi - lo));
+          c = min(max(c, lo + 1u), hi - 1u);
+          --sec;
+        }
+      }
+      // coarse keys per count between the probe and the coarse result
+      // (steering only)
+      if (n1 != xb) {
+        const float so = (float)abs((int)Tk - (int)p1) * rcp_approx((float)abs((int)(n1 - xb)));
+        slope = fmaf(UQ_ENC16_SLOPE_EMA, min(so, 4096.f) - slope, slope);
+      }
+    }
+#else
     float islope;
     {
       const float t = rms * ratio;
@@ -984,6 +1038,7 @@ encode_f32_kernel(const float* __restrict__ u, int64_t n, int32_t d, int64_t ld,
         chi = up_ ? chi : cnt;
       }
     }
+    #endif
     auto c2key = [](uint32_t c) { return __float_as_uint(__half2float(__ushort_as_half((unsigned short)c))); };
     if (exact) {
       Tk = c2key(Tk);                 // keys >= f32(Tc) <=> coarse >= Tc: exactly x of them
@@ -1164,12 +1219,13 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
     return e ? (float)atof(e) : 0.f;
   }();
   const float delta = delta_env > 0.f ? delta_env : (sizeof(T) == 4 ? 0.03f : std::is_same<T, __half>::value ? 0.03f : 0.08f);
+  // initial f16 keys per unit of count near T* for d half-normal magnitudes
+  // of scale s: count density 2 d phi(z) / s per unit value, ~T* 2^-10.5 per
+  // key (f16 ulp) at T* = s z -> 2^10.5 / (2 d phi(z) z); learned per warp
+  // (the f16 search and the f32 coarse search)
+  const double phz = std::exp(-0.5 * (double)z0 * (double)z0) * 0.3989422804014327;
+  const float slope0 = (float)std::min(4096.0, std::max(0.25, 1448.15468787 / (2.0 * d * phz * (double)z0)));
   if constexpr (std::is_same<T, __half>::value) {
-    // initial keys per unit of count near T* for d half-normal magnitudes of
-    // scale s: count density 2 d phi(z) / s per unit value, ~T* 2^-10.5 per
-    // key (f16 ulp) at T* = s z -> 2^10.5 / (2 d phi(z) z); learned per warp
-    const double phz = std::exp(-0.5 * (double)z0 * (double)z0) * 0.3989422804014327;
-    const float slope0 = (float)std::min(4096.0, std::max(0.25, 1448.15468787 / (2.0 * d * phz * (double)z0)));
     z0 *= 1.2533141f;   // the f16 kernel steers by mean |u| = s * sqrt(2 / pi) for N(0, s^2)
     if (vec && d == 256 * NCH)
       encode_f16_kernel<NCH, true, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
@@ -1186,13 +1242,13 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
   if constexpr (std::is_same<T, float>::value) {
     if (vec && d == 128 * NCH)
       encode_f32_kernel<NCH, true, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-          (const float*)u, n, d, ld, x, z0, delta, codes);
+          (const float*)u, n, d, ld, x, z0, delta, slope0, codes);
     else if (vec)
       encode_f32_kernel<NCH, true, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-          (const float*)u, n, d, ld, x, z0, delta, codes);
+          (const float*)u, n, d, ld, x, z0, delta, slope0, codes);
     else
       encode_f32_kernel<NCH, false, false><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
-          (const float*)u, n, d, ld, x, z0, delta, codes);
+          (const float*)u, n, d, ld, x, z0, delta, slope0, codes);
     note_launch();
     return cudaGetLastError();
   }
