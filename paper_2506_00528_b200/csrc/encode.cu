@@ -864,6 +864,244 @@ encode_f16_kernel(const __half* __restrict__ u, int64_t n, int32_t d, int64_t ld
 }
 
 // ---------------------------------------------------------------------------
+// fp16 rows, large n: R rows per warp iteration (a BATCH), the same exact
+// search as encode_f16_kernel with its CONTROL run lane-parallel.  The search
+// above spends ~75 warp instructions per count pass of which 26 count; the
+// rest -- bracket update, interpolation, clamps, branches -- is warp-uniform
+// scalar work.  Here lane r (< R) owns the search state of the batch's row r:
+// one round is, for every row still searching, {broadcast its threshold (one
+// SHFL), count over the row (the same biased HSET2/HADD2 sums + REDUX), keep
+// the count in lane r}, then ONE lane-parallel bracket update / next
+// threshold for all R rows at once.  A warp cannot hold R rows in registers,
+// so the batch is staged in shared memory by cp.async (16 B per lane per
+// chunk, each lane reads back only what it staged itself: no barriers, no bank
+// conflicts) and each pass re-reads its row with NCH LDS.128.  T*/scale and the
+// count slope are learned per lane (each lane sees every R-th row of the warp).
+// Every decision is the same exact f16 compare as above: identical bytes.
+#ifndef UQ_ENC16_BATCH
+#define UQ_ENC16_BATCH 0
+#endif
+#ifndef UQ_ENC16_BATCH_R
+#define UQ_ENC16_BATCH_R 8
+#endif
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+  return v;
+}
+
+template <int NCH, int R>
+__global__ void __launch_bounds__(kEncWarps * 32, R >= 8 ? 2 : 4)
+encode_f16_batch_kernel(const __half* __restrict__ u, int64_t n, int64_t ld, int32_t x, float z0, float slope0,
+                        uint8_t* __restrict__ codes) {
+  extern __shared__ __align__(16) uint8_t enc_smem[];
+  constexpr int NW = 4 * NCH;
+  constexpr int NS = NCH < 2 ? NCH : 2;
+  constexpr uint32_t kEnd = 0x7c01u;
+  constexpr int64_t pb = 32 * NCH, cb = 2 * pb;
+  constexpr uint32_t kRowBytes = 512u * NCH;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (int64_t)blockIdx.x * kEncWarps + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * kEncWarps;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(enc_smem) + (threadIdx.x >> 5) * (R * kRowBytes) + lane * 16;
+  const float inv_ns = 1.0f / (float)(256 * NS);
+  const unsigned xb = (unsigned)x + kF16Bias;
+  float ratio = z0, slope = slope0;   // per lane: learned over the rows this lane owns
+  const int64_t nbatch = (n + R - 1) / R;
+  for (int64_t b = warp_global; b < nbatch; b += nwarps) {
+    const int64_t row0 = b * R;
+    const int nr = (int)min((int64_t)R, n - row0);
+    const __half* ub = u + row0 * ld;
+    // L2 prefetch of this warp's next batch, one 128-byte line per lane and step
+    if (b + nwarps < nbatch) {
+      const __half* un = ub + nwarps * R * ld;
+      const int nrn = (int)min((int64_t)R, n - (row0 + nwarps * R));
+#pragma unroll
+      for (int t = 0; t < (R * NCH * 4 + 31) / 32; ++t) {
+        const int li = t * 32 + lane, pr = li / (NCH * 4), pl = li % (NCH * 4);
+        if (pr < nrn) asm volatile("prefetch.global.L2 [%0];" ::"l"(un + pr * ld + pl * 64) : "memory");
+      }
+    }
+    // ---- stage the batch: lane l keeps 16 B of every 512-B chunk ----
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nr) {
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) cp_async16(sbase + r * kRowBytes + j * 512, ub + r * ld + j * 256 + lane * 8);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+
+    // ---- row scales: mean |u| over the first NS chunks (steering only) ----
+    int ssi = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nr) {
+        __half2 acc = __float2half2_rn(0.f);
+        const __half2 sc = __float2half2_rn(0.015625f);
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          const uint4 v = lds128(sbase + r * kRowBytes + j * 512);
+          acc = __hfma2(__habs2(h2(v.x)), sc, acc);
+          acc = __hfma2(__habs2(h2(v.y)), sc, acc);
+          acc = __hfma2(__habs2(h2(v.z)), sc, acc);
+          acc = __hfma2(__habs2(h2(v.w)), sc, acc);
+        }
+        const float ss = (__low2float(acc) + __high2float(acc)) * 64.f;
+        const int tot = (int)redux_add((unsigned)min(__float2int_rn(ss * 1024.f), 1 << 26));
+        if (lane == r) ssi = tot;
+      }
+    }
+    const float rms = (float)ssi * (inv_ns * (1.f / 1024.f));
+
+    // ---- lane r: search state of row r ----
+    const bool owner = lane < nr;
+    uint32_t lo = 0u, hi = kEnd, Tk = 0u;
+    unsigned clo = 256u * NCH + kF16Bias, chi = kF16Bias;
+    bool exact = false, done = !owner;
+    const uint32_t p1 =
+        min(max((uint32_t)__half_as_ushort(__float2half_rn(rms * ratio)) & 0x7fffu, 1u), 0x7bffu);
+    uint32_t c = p1;
+    unsigned n1 = xb, sec = 6u;
+    float islope = slope;
+    bool first = true;
+    unsigned act = __ballot_sync(kFull, !done);
+    while (act != 0u) {
+      unsigned cnt = 0u;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (act & (1u << r)) {
+          const uint32_t c2 = dup16(__shfl_sync(kFull, c, r));
+          uint32_t w[NW];
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            const uint4 v = lds128(sbase + r * kRowBytes + j * 512);
+            w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+          }
+          const unsigned cr = f16_count_ge<NW>(w, c2);
+          if (lane == r) cnt = cr;
+        }
+      }
+      if (!done) {
+        if (first) {
+          // the probe at the predicted T*, then a step by the learned slope
+          n1 = cnt;
+          if (n1 == xb) { Tk = p1; exact = true; done = true; }
+          else {
+            const bool up1 = n1 > xb;
+            lo = up1 ? p1 : 0u; clo = up1 ? n1 : clo;
+            hi = up1 ? kEnd : p1; chi = up1 ? chi : n1;
+            c = (uint32_t)((int)p1 + __float2int_rn((float)(int)(n1 - xb) * slope));
+            c = (int)c <= (int)lo ? lo + 1u : min(c, hi - 1u);
+          }
+        } else {
+          exact = cnt == xb;
+          const bool up_ = cnt > xb;
+          Tk = c;
+          lo = up_ ? c : lo;
+          clo = up_ ? cnt : clo;
+          hi = up_ ? hi : c;
+          chi = up_ ? chi : cnt;
+          if (exact || hi - lo <= 1u) done = true;
+          else if (hi == kEnd || lo == 0u) {
+            const uint32_t s = (uint32_t)(((float)(hi == kEnd ? clo - xb : xb - chi) + 0.5f) * islope) + 1u;
+            c = hi == kEnd ? lo + s : (hi > s ? hi - s : 0u);
+            c = min(max(c, lo + 1u), hi - 1u);
+            islope *= 2.f;
+          } else if (sec == 0u) {
+            c = lo + ((hi - lo) >> 1);
+            sec = 1u;
+          } else {
+            const float f = ((float)(clo - xb) + UQ_ENC16_OFF) * rcp_approx((float)(clo - chi));
+            c = lo + (uint32_t)(f * (float)(hi - lo));
+            c = min(max(c, lo + 1u), hi - 1u);
+            --sec;
+          }
+        }
+      }
+      first = false;
+      act = __ballot_sync(kFull, !done);
+    }
+    if (owner) {
+      if (!exact) { Tk = lo; exact = (clo == xb); }
+      if (Tk != 0u && rms > 0.f) {
+        const float rn = __fdividef(ElemBits<__half>::key2f(Tk), rms);
+        if (rn > 0.f && rn < 1e30f) ratio = fmaf(UQ_ENC16_EMA, rn - ratio, ratio);
+      }
+      if (n1 != xb) {
+        const float so = (float)abs((int)Tk - (int)p1) * rcp_approx((float)abs((int)(n1 - xb)));
+        slope = fmaf(UQ_ENC16_SLOPE_EMA, min(so, 4096.f) - slope, slope);
+      }
+    }
+
+    // ---- plane bytes, row by row ----
+    const uint32_t tkx = Tk | (exact ? 0x80000000u : 0u);
+    uint8_t* cp = codes + row0 * cb;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nr) {
+        const uint32_t tr = __shfl_sync(kFull, tkx, r);
+        const uint32_t Tr = tr & 0x7fffffffu;
+        uint32_t w[NW];
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const uint4 v = lds128(sbase + r * kRowBytes + j * 512);
+          w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+        }
+        uint32_t posb[NCH], negb[NCH];
+        if ((tr >> 31) != 0u || Tr == 0u) {
+          const uint32_t ts = (Tr == 0u) ? 1u : Tr;
+          const __half2 tp = h2(dup16(ts)), tn = h2(dup16(ts | 0x8000u));
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            posb[j] = bits8_bf(__hge2(h2(w[4 * j]), tp), __hge2(h2(w[4 * j + 1]), tp),
+                               __hge2(h2(w[4 * j + 2]), tp), __hge2(h2(w[4 * j + 3]), tp));
+            negb[j] = bits8_bf(__hle2(h2(w[4 * j]), tn), __hle2(h2(w[4 * j + 1]), tn),
+                               __hle2(h2(w[4 * j + 2]), tn), __hle2(h2(w[4 * j + 3]), tn));
+          }
+        } else {
+          // ties at T*: keys > T plus the first x - count(> T) keys == T in index order (R1)
+          const __half2 tp = h2(dup16(Tr)), tn = h2(dup16(Tr | 0x8000u));
+          int need = (int)(xb - __shfl_sync(kFull, chi, r));
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            const uint32_t gp = mask8(__hgt2_mask(h2(w[4 * j]), tp), __hgt2_mask(h2(w[4 * j + 1]), tp),
+                                      __hgt2_mask(h2(w[4 * j + 2]), tp), __hgt2_mask(h2(w[4 * j + 3]), tp)) & 0xffu;
+            const uint32_t gn = mask8(__hlt2_mask(h2(w[4 * j]), tn), __hlt2_mask(h2(w[4 * j + 1]), tn),
+                                      __hlt2_mask(h2(w[4 * j + 2]), tn), __hlt2_mask(h2(w[4 * j + 3]), tn)) & 0xffu;
+            const uint32_t ep = mask8(__heq2_mask(h2(w[4 * j]), tp), __heq2_mask(h2(w[4 * j + 1]), tp),
+                                      __heq2_mask(h2(w[4 * j + 2]), tp), __heq2_mask(h2(w[4 * j + 3]), tp)) & 0xffu;
+            const uint32_t en = mask8(__heq2_mask(h2(w[4 * j]), tn), __heq2_mask(h2(w[4 * j + 1]), tn),
+                                      __heq2_mask(h2(w[4 * j + 2]), tn), __heq2_mask(h2(w[4 * j + 3]), tn)) & 0xffu;
+            uint32_t eq = ep | en;
+            const int ce = __popc(eq);
+            int incl = ce;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int tv = __shfl_up_sync(kFull, incl, o);
+              if (lane >= o) incl += tv;
+            }
+            const int take = min(max(need - (incl - ce), 0), ce);
+            while (__popc(eq) > take) eq &= ~(0x80000000u >> __clz(eq));
+            need -= __shfl_sync(kFull, incl, 31);
+            posb[j] = gp | (eq & ep);
+            negb[j] = gn | (eq & en);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          cp[r * cb + 32 * j + lane] = (uint8_t)posb[j];
+          cp[r * cb + pb + 32 * j + lane] = (uint8_t)negb[j];
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // f32 rows (c2-c4 DB encodes): the f16 kernel's structure on the f32 search.
 // The generic kernel spent ~850 warp instructions per d=768 row (ncu: ALU pipe
 // 78%, issue 77%; profiles/r02/enc_f32_*).  Here:
@@ -1227,6 +1465,26 @@ static cudaError_t launch_encode_nch(const void* u, int64_t n, int32_t d, int64_
   const float slope0 = (float)std::min(4096.0, std::max(0.25, 1448.15468787 / (2.0 * d * phz * (double)z0)));
   if constexpr (std::is_same<T, __half>::value) {
     z0 *= 1.2533141f;   // the f16 kernel steers by mean |u| = s * sqrt(2 / pi) for N(0, s^2)
+#if UQ_ENC16_BATCH
+    if constexpr (NCH <= 4) {
+      // large n: the batched kernel (R rows per warp iteration, lane-parallel
+      // search control); small n keeps one row per warp (more warps in flight)
+      constexpr int R = NCH <= 3 ? UQ_ENC16_BATCH_R : (UQ_ENC16_BATCH_R < 4 ? UQ_ENC16_BATCH_R : 4);
+      constexpr int kSmem = kEncWarps * R * 512 * NCH;
+      constexpr int kCtas = R >= 8 ? 2 : 4;
+      if (vec && d == 256 * NCH && n >= (int64_t)sms * kCtas * kEncWarps * R) {
+        static const cudaError_t attr = cudaFuncSetAttribute(encode_f16_batch_kernel<NCH, R>,
+                                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (attr != cudaSuccess) return attr;
+        const int64_t nb = (n + R - 1) / R;
+        const int64_t bl = std::min<int64_t>((nb + kEncWarps - 1) / kEncWarps, (int64_t)sms * kCtas);
+        encode_f16_batch_kernel<NCH, R><<<(unsigned)bl, kEncWarps * 32, kSmem, st>>>(
+            (const __half*)u, n, ld, x, z0, slope0, codes);
+        note_launch();
+        return cudaGetLastError();
+      }
+    }
+#endif
     if (vec && d == 256 * NCH)
       encode_f16_kernel<NCH, true, true><<<(unsigned)blocks, kEncWarps * 32, 0, st>>>(
           (const __half*)u, n, d, ld, x, z0, delta, slope0, codes);

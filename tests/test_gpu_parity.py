@@ -178,6 +178,36 @@ def test_encode_f16_row_pairs(uq, orc, d):
             assert bad.size == 0, (d, n, x, bad)
 
 
+@pytest.mark.parametrize("d", [256, 512, 768, 1024])
+def test_encode_f16_batched_rows(uq, orc, d):
+    """fp16 rows with d = 256k and n above ~19k run the batched kernel (8 or 4
+    rows per warp iteration staged in shared memory, lane r owning row r's
+    search): a ragged row count (last batch partial, rows 1..7 of it), batches
+    whose rows take different paths and different pass counts (exact at the
+    probe / ties / T* = 0 / extrapolation far outside the learned ratio /
+    subnormal and near-maximum scales / binade-edge ties), and a small-n call
+    (one row per warp kernel) that must return the same bytes."""
+    rng = np.random.default_rng(d + 77)
+    n = 20011
+    u = rng.standard_normal((n, d)).astype(np.float32)
+    u[1::5] = _tie_heavy(rng, len(u[1::5]), d)
+    u[2::7] *= np.float32(2.0) ** rng.integers(-22, 14, (len(u[2::7]), 1))
+    u[3::11] = 0.0
+    u[3::11, ::5] = 1.0
+    u[4::13] = np.sign(u[4::13]) * np.float32(2.0) ** rng.integers(-3, 4, u[4::13].shape)
+    u[6::17] = 0.0
+    u[9::19] = np.float32(0.5)
+    ut = torch.from_numpy(u).to(torch.float16)
+    host = ut.numpy()
+    for x in sorted({1, d // 4, d // 2, d - 1, d}):
+        got = uq.encode(ut.cuda(), x).cpu().numpy()
+        ref = orc.pack(orc.encode(host, x))
+        bad = np.argwhere((got != ref).any(1))[:5].ravel()
+        assert bad.size == 0, (d, x, bad)
+        small = uq.encode(ut[:1003].cuda(), x).cpu().numpy()
+        assert np.array_equal(small, ref[:1003]), (d, x)
+
+
 def test_encode_c5_fp16_unnormalised(uq, orc):
     """Config 5 recipe (fp16, raw mixture values; ~10% of rows tie at the top-x boundary)."""
     w = datagen.CONFIGS["c5"].scaled(n=20000, nq=16)
