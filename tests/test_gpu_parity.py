@@ -180,9 +180,11 @@ def test_encode_f16_row_pairs(uq, orc, d):
 
 @pytest.mark.parametrize("d", [256, 512, 768, 1024])
 def test_encode_f16_batched_rows(uq, orc, d):
-    """fp16 rows with d = 256k and n above ~19k run the batched kernel (8 or 4
-    rows per warp iteration staged in shared memory, lane r owning row r's
-    search): a ragged row count (last batch partial, rows 1..7 of it), batches
+    """Large-n fp16 encodes with d = 256k: the shape the batched kernel serves
+    when the library is built with -DUQ_ENC16_BATCH=1 (8 or 4 rows per warp
+    iteration staged in shared memory, lane r owning row r's search; measured
+    slower and compiled out by default, DESIGN.md section 7 -- the default
+    build runs the one-row-per-warp kernel here): a ragged row count (last batch partial, rows 1..7 of it), batches
     whose rows take different paths and different pass counts (exact at the
     probe / ties / T* = 0 / extrapolation far outside the learned ratio /
     subnormal and near-maximum scales / binade-edge ties), and a small-n call
